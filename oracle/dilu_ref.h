@@ -1,0 +1,97 @@
+/*
+ * dilu_ref.h -- CPU ORACLE for the Dilu introspective-elasticity provisioning loop.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2503_05130_b200/, include/dilu.h) never links, imports or calls it, and
+ * shares no code, header, table or helper with it.
+ *
+ * What it computes: SURVEY.md s8(c) steps 1-10, which restate the paper's
+ *   - Algorithm 1 ScheduleInstances / SelectOptGPU   (s3.3)
+ *   - Principle 1-3 (affinity first, best-fit / LLM worst-fit, Omega/gamma caps)
+ *                                                     (s3.3)
+ *   - slot-level reading of Algorithm 2 IssueToken    (s3.4.1)
+ *   - lazy scale-out/in on a 40 s window              (s3.4.2)
+ *   - the SVR / CSC / fragmentation / throughput tallies
+ * in integer quota units, one plain loop per step, in the
+ * paper's order.  Readings of silent/ambiguous passages are DESIGN.md s3 (Q1-Q27).
+ *
+ * Struct layouts are declared here independently of include/dilu.h: both are a flat
+ * sequence of int32 fields in the order the seeded input generator (dilu_inputs/)
+ * writes, so the same numpy buffers feed both sides.
+ */
+#ifndef DILU_REF_H
+#define DILU_REF_H
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  REF_OK = 0, REF_E_USAGE = 1, REF_E_INVARIANT = 2, REF_E_IO = 3,
+  REF_E_CUDA = 4, REF_E_STATE = 5, REF_E_CAPACITY = 6
+};
+
+#define REF_NT 17  /* tally vector length */
+
+typedef struct {
+  int32_t n_scenarios, gpus_per_scenario, max_funcs, max_instances;
+  int32_t q_pm, mem_mib, omega_pm, gamma_pm, alpha_w, beta_w, slot_ms;
+  int32_t window_s, phi_out, phi_in, min_instances, max_residents, max_llm_stages;
+  int32_t n_patterns, pattern_len, flags;           /* flags bit0 LLM split, bit1 invariants */
+} ref_config;
+
+typedef struct { int32_t scenario_id, omega_pm, gamma_pm, reserved; } ref_scenario;
+
+typedef struct {
+  int32_t kind, prio, ibs, req_pm, lim_pm, mem_mib, work_per_batch, n_workers;
+  int32_t duty_pm, cold_slots, affinity_class, arrive_sec, depart_sec;
+  int32_t pattern, scale_q10, phase_slots;
+} ref_func;
+
+typedef struct ref_sim ref_sim;
+
+/* whole-loop API (mirrors the product C-ABI shape under a dilu_ref_ prefix) */
+int32_t dilu_ref_create(const ref_config* cfg, const ref_scenario* scen /* [S] or NULL */,
+                        const ref_func* funcs /* [S*F] */, const int32_t* patterns,
+                        ref_sim** out);
+int32_t dilu_ref_place_batch(ref_sim* s, int32_t n_req, const int32_t* req_scenario,
+                             const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid);
+int32_t dilu_ref_scale_step(ref_sim* s, int32_t n_slots, int32_t n_threads);
+int32_t dilu_ref_metrics(ref_sim* s, int64_t* per_scenario /* [S][17] or NULL */, int64_t* sum /* [17] */);
+int32_t dilu_ref_snapshot(ref_sim* s, int32_t id_cap, int32_t* gpu /* [S][G][4] */,
+                          int32_t* inst /* [S][id_cap][12] */);
+int32_t dilu_ref_slot(const ref_sim* s);
+/* last simulated slot of one scenario: a[id][stage] allocated tokens, r[id]
+ * dispatched requests, exec[g] executed tokens (0 for cold / idle). */
+int32_t dilu_ref_slot_detail(ref_sim* s, int32_t scenario, int32_t id_cap, int64_t* a,
+                             int32_t* r, int64_t* exec);
+const char* dilu_ref_last_error(const ref_sim* s);
+void dilu_ref_destroy(ref_sim* s);
+
+/* unit steps, exported so tests can pin each one on its own; the loop above calls
+ * exactly these functions */
+uint64_t dilu_ref_mix(uint64_t scn, uint64_t t, uint64_t i, uint64_t g, uint64_t a);
+int64_t dilu_ref_cap1(int32_t slot_ms, int32_t req_pm, int32_t c_b, int32_t ibs);
+int32_t dilu_ref_select_opt_gpu(int32_t n_cand, const int32_t* cand, const int32_t* R,
+                                const int32_t* L, const int32_t* U, const int32_t* nres,
+                                int32_t req, int32_t lim, int32_t mem, int32_t omega_u,
+                                int32_t gamma_u, int32_t M, int32_t Q, int32_t a, int32_t b);
+void dilu_ref_vertical_row(int32_t n, const int32_t* prio, const int32_t* id,
+                           const int64_t* req_tok, const int64_t* lim_tok, const int64_t* d,
+                           int64_t T_slot, int64_t* a_out);
+int32_t dilu_ref_scaling_decision(int32_t W, const int32_t* window, int32_t n, int64_t cap1,
+                                  int32_t phi_out, int32_t phi_in, int32_t min_instances,
+                                  int32_t* k_out);
+int32_t dilu_ref_llm_split(int32_t n_gpu, const int32_t* active, const int32_t* R,
+                           const int32_t* L, const int32_t* U, const int32_t* nres,
+                           const int32_t* excluded, int32_t req, int32_t lim, int32_t mem,
+                           int32_t omega_u, int32_t gamma_u, int32_t M, int32_t max_stages,
+                           int32_t* out_g, int32_t* out_share);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
