@@ -1,0 +1,177 @@
+/*
+ * dilu.h -- C-ABI of libdilu.so, the B200 (sm_100a) implementation of the batched
+ * Dilu introspective-elasticity provisioning loop (arXiv 2503.05130).
+ *
+ * One handle simulates n_scenarios independent synthetic clusters ("scenarios")
+ * slot by slot.  Each slot does:
+ *   - at second boundaries: window push, departures, lazy horizontal scaling
+ *     (s3.4.2), function arrivals, and one FIFO placement pass
+ *     of Algorithm 1 (s3.3) with Principle 1-3;
+ *   - every slot: arrivals and dispatch, token-based vertical scaling -- request
+ *     floor plus the spare shared up to each limit, SLO-sensitive first
+ *     (slot-level reading of Algorithm 2, s3.4.1) -- the gang
+ *     minima of training jobs (barrel effect) and the metric fold.
+ * All quantities are integers (R1-R8 in DESIGN.md s3); outputs are bit-exact and
+ * independent of launch shape, device count and run.
+ *
+ * Conventions
+ *   - Every call returns dilu_status; no C++ exception crosses this boundary.
+ *   - "d_" pointers are device memory on the handle's device; "h_" pointers are
+ *     host memory read only during the call.  dilu_metrics accepts either kind.
+ *   - The workspace is caller-owned (e.g. a torch uint8 tensor) of at least
+ *     dilu_workspace_bytes(cfg) bytes, 256-byte aligned; the handle borrows it until
+ *     dilu_sim_destroy.  The stream is caller-owned (cudaStream_t, may be 0).
+ *   - A handle is not thread-safe; handles are independent of each other.
+ *   - Capacity exhaustion of a placement is a per-request result (-1), not an error.
+ *   - Launches are stream-ordered and asynchronous except dilu_metrics and
+ *     dilu_snapshot, which synchronise the stream and surface deferred errors.
+ */
+#ifndef DILU_H
+#define DILU_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t dilu_status;
+enum {
+  DILU_OK = 0,
+  DILU_E_USAGE = 1,      /* invalid argument / validation failure (SPEC exit 1)      */
+  DILU_E_INVARIANT = 2,  /* debug invariant check failed (SPEC exit 2)                      */
+  DILU_E_IO = 3,         /* reserved (SPEC exit 3)                                          */
+  DILU_E_CUDA = 4,       /* CUDA launch / runtime error                                     */
+  DILU_E_STATE = 5,      /* call out of order, or handle already failed                     */
+  DILU_E_CAPACITY = 6    /* live instances of a scenario exceeded cfg.max_instances         */
+};
+
+#define DILU_NT 17  /* tally vector length */
+enum {
+  DILU_T_GPU_SLOTS_ACTIVE = 0,  /* sum over slots of #active GPUs (Eq.1 g_i)        */
+  DILU_T_SM_UNUSED = 1,         /* sum over active GPU-slots of T_slot - executed tokens    */
+  DILU_T_MEM_UNUSED = 2,        /* sum over active GPU-slots of M - U_g (MiB)               */
+  DILU_T_REQ_TOTAL = 3,
+  DILU_T_REQ_SERVED = 4,
+  DILU_T_REQ_VIOLATED = 5,      /* capacity-SVR numerator (Q17)                             */
+  DILU_T_INF_EXEC = 6,          /* executed inference tokens                                */
+  DILU_T_TRAIN_PROGRESS = 7,    /* n_workers * gang minimum, summed (Q22)                   */
+  DILU_T_PLACEMENTS_OK = 8,
+  DILU_T_PLACEMENT_FAILURES = 9,
+  DILU_T_COLD_STARTS = 10,      /* CSC (Q20)                                                */
+  DILU_T_SCALE_OUT = 11,
+  DILU_T_SCALE_IN = 12,
+  DILU_T_LLM_SPLIT = 13,
+  DILU_T_ALLOC_HASH = 14,       /* uint64 wrap-sum of mix(scn,t,i,g,a) over warm residents  */
+  DILU_T_GPU_ROW_SLOTS = 15,    /* G * slots = simulated GPU-slot decisions                 */
+  DILU_T_MAX_ACTIVE = 16        /* per-scenario max #active; the scenario sum adds maxima   */
+};
+
+/* Scenario-independent configuration, all integer units (R1-R5). */
+typedef struct {
+  int32_t n_scenarios;        /* scenarios in this handle (>= 1)                           */
+  int32_t gpus_per_scenario;  /* G, 1..32767 on this implementation                        */
+  int32_t max_funcs;          /* F: profile-table rows per scenario                        */
+  int32_t max_instances;      /* live (placed + pending) instances per scenario            */
+  int32_t q_pm;               /* SM_total in per-mille; must be 1000 (R1)                  */
+  int32_t mem_mib;            /* M, memory per GPU in MiB (R2), <= 2^20                    */
+  int32_t omega_pm, gamma_pm; /* defaults for Omega, gamma when scen == NULL       */
+  int32_t alpha_w, beta_w;    /* integer score weights a:b = alpha:beta (R6), 0..255       */
+  int32_t slot_ms;            /* slot length; divides 1000. T_slot = 1000*slot_ms tokens   */
+  int32_t window_s, phi_out, phi_in, min_instances; /* 40, 20, 30, 1           */
+  int32_t max_residents;      /* must be 32                                                */
+  int32_t max_llm_stages;     /* 1..4                                             */
+  int32_t n_patterns, pattern_len;
+  int32_t flags;              /* bit0: LLM worst-fit split enabled                         */
+} dilu_config;
+
+/* Per-scenario parameters (the C4 sweep varies gamma per scenario). */
+typedef struct {
+  int32_t scenario_id;        /* global id, feeds alloc_hash so shards sum identically     */
+  int32_t omega_pm, gamma_pm;
+  int32_t reserved;
+} dilu_scenario;
+
+/* One quantised profile-table row <IBS, request, limit, memory> plus lifecycle
+ * (Table 1).  kind -1 marks an unused row. */
+typedef struct {
+  int32_t kind;            /* 0 inference, 1 LLM inference, 2 training, -1 unused          */
+  int32_t prio;            /* 0 SLO-sensitive, 1 best-effort (Alg.2 Type)           */
+  int32_t ibs, req_pm, lim_pm, mem_mib;
+  int32_t work_per_batch;  /* c_b tokens = req_pm * SLO_ms / 2 (R4); 0 for training        */
+  int32_t n_workers;       /* n_j GPUs of a training job (Alg.1)                    */
+  int32_t duty_pm;         /* training compute duty (comm idle)                     */
+  int32_t cold_slots, affinity_class, arrive_sec, depart_sec;
+  int32_t pattern, scale_q10, phase_slots;  /* A_f(t) = pat[p][(t+phase)%T] * scale >> 10 */
+} dilu_func;
+
+typedef struct dilu_sim dilu_sim;
+
+/* Bytes of device workspace a handle needs for cfg (0 if cfg is invalid). */
+size_t dilu_workspace_bytes(const dilu_config* cfg);
+
+/* Validate the inputs (first violation named in *out's last error, or on stderr if
+ * *out cannot be created), copy them H->D into the workspace on the stream, and
+ * initialise every scenario at slot 0 (no function registered, all GPUs inactive).
+ *   cfg      host, read during the call
+ *   h_scen   host [n_scenarios] or NULL (then ids 0.. and cfg's Omega/gamma)
+ *   h_funcs  host [n_scenarios * max_funcs]
+ *   h_patterns host int32 [n_patterns * pattern_len]
+ * Errors: DILU_E_USAGE (validation, workspace too small/misaligned), DILU_E_CUDA. */
+dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
+                            const dilu_func* h_funcs, const int32_t* h_patterns,
+                            void* d_workspace, size_t ws_bytes, void* cuda_stream,
+                            dilu_sim** out);
+
+/* Return every scenario to slot 0 with the inputs already resident (no H->D copy). */
+dilu_status dilu_sim_reset(dilu_sim* s);
+
+/* Explicit deployment requests at the current slot (Alg.1 "Accept the deployment
+ * request for F_j"): request j deploys one request of function
+ * d_req_func[j] in scenario d_req_scenario[j] (a gang of n_workers for training,
+ * one instance otherwise), registering the function if needed; requests are
+ * enqueued in array order per scenario, then one FIFO placement pass runs over every
+ * scenario's whole queue.  Outputs per request: GPU of its first instance or -1 if
+ * it stays queued ("-1"), and its first instance id.  All four arrays are
+ * device int32 [n_req]; n_req may be 0 (just run the pass).                        */
+dilu_status dilu_place_batch(dilu_sim* s, int32_t n_req, const int32_t* d_req_scenario,
+                             const int32_t* d_req_func, int32_t* d_out_gpu, int32_t* d_out_iid);
+
+/* Advance all scenarios by n_slots slots (boundary work included); stream-ordered,
+ * no host synchronisation. */
+dilu_status dilu_scale_step(dilu_sim* s, int32_t n_slots);
+
+/* Reduce tallies: per-scenario int64 [n_scenarios][DILU_NT] (may be NULL) and the
+ * scenario sum int64 [DILU_NT] (uint64 wrap-sum for the hash, may be NULL).  Pointers
+ * may be host or device (copied with cudaMemcpyDefault).  Synchronises the stream and
+ * returns any deferred DILU_E_CAPACITY / DILU_E_CUDA. */
+dilu_status dilu_metrics(dilu_sim* s, int64_t* per_scenario, int64_t* sum);
+
+/* Parity helper (off the timed path): device outputs
+ *   d_gpu  int32 [n_scenarios][G][4]        = R_g, L_g, U_g, |res_g|
+ *   d_inst int32 [n_scenarios][id_cap][12]  = per instance id: func, status
+ *          (0 pending, 1 placed, 2 terminated, -1 never issued), n_stages,
+ *          ready_slot, gpu[4], mem_share[4] (-1 / 0 when not placed).
+ * Synchronises the stream. */
+dilu_status dilu_snapshot(dilu_sim* s, int32_t id_cap, int32_t* d_gpu, int32_t* d_inst);
+
+/* Diagnostics (tracing; off the timed path): per-scenario int64 [n_scenarios][8] (may
+ * be NULL) and their sum [8] (may be NULL) of kernel counters accumulated since the
+ * last create/reset: full placement attempts, retry-skip checks, row repacks, boundary
+ * events, queue scans, slots simulated, 2 reserved.  Host or device pointers.
+ * Synchronises the stream. */
+dilu_status dilu_kernel_stats(dilu_sim* s, int64_t* per_scenario, int64_t* sum);
+
+/* Current slot (number of slots simulated so far). */
+int32_t dilu_current_slot(const dilu_sim* s);
+
+/* Last error message, owned by the handle, valid until the next call. */
+const char* dilu_last_error(const dilu_sim* s);
+
+/* Release the handle (not the caller-owned workspace or stream). */
+void dilu_sim_destroy(dilu_sim* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DILU_H */

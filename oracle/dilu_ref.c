@@ -956,7 +956,7 @@ int32_t dilu_ref_snapshot(ref_sim* s, int32_t id_cap, int32_t* gpu, int32_t* ins
           continue;
         }
         RInst* I = &sc->inst[id];
-        o[0] = I->func;
+        o[0] = I->status == ST_TERMINATED ? -1 : I->func;   /* ABI: -1 once terminated */
         o[1] = I->status;
         o[2] = I->status == ST_PLACED ? I->nst : 0;
         o[3] = I->status == ST_PLACED ? I->ready : -1;

@@ -1,0 +1,1131 @@
+// sim_kernel.cuh -- the B200 megakernel for the batched Dilu provisioning loop.
+//
+// Grid: one CTA per scenario (scenarios are independent); the CTA runs
+// every slot of the call.  Per slot:
+//   boundary (t % SPS == 0):
+//     B1  function-parallel: window push + incremental lazy-scaling counts and
+//         decisions, departure/arrival flags; ordered compaction of the
+//         functions with an event
+//     B3  thread 0 applies events in the paper's order: departures, ScaleOut/In,
+//         arrivals (ids assigned at enqueue)
+//     B4  FIFO placement pass, Alg.1: per instance, every thread scores a
+//         stride of GPUs with a packed 64-bit key (tier | fit | id), block min, thread
+//         0 commits.  LLM worst-fit split by <=4 block argmax rounds.
+//     B5  repack GPU rows into warp chunks when the residency changed
+//   P0  function-parallel: arrivals A_f(t), even dispatch over warm instances
+//   P1  warp chunks of GPU rows (rows of width w in {1..32} lanes): slot-level Alg.2
+//       allocation a = req + min(want, max(0, S_g - prefix)) with width-w segmented
+//       shuffles, executed batches, hash, gang/stage minima via shared atomics
+//   P2  function-parallel: training gangs (barrel effect) and LLM stage minima
+// Tallies accumulate in registers and are block-reduced once per call.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "state.cuh"
+
+namespace dilu {
+
+struct Params {
+  const int32_t* funcs;      // [S][F][16] input rows
+  const int32_t* pat;        // [P][Tp]
+  const int32_t* scen;       // [S][4]
+  uint8_t* state;            // [S][L.bytes]
+  int32_t* ring;             // [S][F][W]
+  int64_t* tally;            // [S][NT]
+  int64_t* stats;            // [S][NSTAT] kernel statistics
+  Layout L;
+  int32_t S, G, F, I, W, M, Q, aw, bw, slot_ms, SPS, phi_out, phi_in, min_inst, max_stages,
+      flags, Tp;
+  int64_t T_slot;
+};
+
+struct Acc0 {  // thread-0 tallies, kept in shared memory (not in every thread's registers)
+  long long act, memu, rows, pok, pfail, cold, sout, sin, split, maxa;
+  long long st[NSTAT];   // statistics: attempts, hope checks, relayouts, events, scanned, slots
+};
+enum { S_ATTEMPT = 0, S_HOPE, S_LAYOUT, S_EVENT, S_SCAN, S_SLOT };
+struct Acc {   // per-thread tallies
+  long long rtot, rsrv, rvio, iexe, tprg, etot;
+  unsigned long long hash;
+  Acc0* z;     // shared, written by thread 0 only
+};
+
+__device__ __forceinline__ uint64_t sm64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t mix5(uint32_t scn, uint32_t t, uint32_t i, uint32_t g,
+                                         uint32_t a) {
+  uint64_t h = sm64(scn);
+  h = sm64(h ^ t);
+  h = sm64(h ^ i);
+  return sm64(h ^ ((uint64_t(g) << 32) | a));
+}
+
+// ---------------------------------------------------------------- block helpers
+
+struct Red {                 // reduction scratch (static shared)
+  unsigned long long u64[2][32];
+  int32_t i32[2][33];
+  long long acc[10][32];
+  int32_t flag;
+  int32_t members[64];       // gang member slots of the request being placed
+  Acc0 z;
+};
+
+// One-sync block min; double-buffered so back-to-back calls do not race.
+__device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v, Red& r,
+                                                            int& phase) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long y = __shfl_xor_sync(0xffffffffu, v, o);
+    v = y < v ? y : v;
+  }
+  unsigned long long* buf = r.u64[phase];
+  phase ^= 1;
+  if (lane == 0) buf[wid] = v;
+  __syncthreads();
+  unsigned long long m = lane < nw ? buf[lane] : ~0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
+    m = y < m ? y : m;
+  }
+  return m;
+}
+
+// One-sync block exclusive scan of int32; returns exclusive prefix, *total.
+__device__ __forceinline__ int32_t block_scan_i32(int32_t v, Red& r, int& phase,
+                                                  int32_t* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  int32_t* buf = r.i32[phase];
+  phase ^= 1;
+  if (lane == 31) buf[wid] = x;
+  __syncthreads();
+  int32_t before = 0, tot = 0;
+  for (int k = 0; k < nw; ++k) {
+    if (k < wid) before += buf[k];
+    tot += buf[k];
+  }
+  *total = tot;
+  return before + x - v;
+}
+
+// ------------------------------------------------------------------ scenario
+
+struct Scn {
+  View& v;                   // lives in shared memory (one per CTA), not in registers
+  const Params* P;
+  const int32_t* frow;       // this scenario's input function rows [F][16]
+  int32_t scn_id, om, ga;
+};
+
+__device__ __forceinline__ int st_of(int32_t meta) { return meta & 3; }
+__device__ __forceinline__ int nst_of(int32_t meta) { return (meta >> 4) & 7; }
+__device__ __forceinline__ bool is_inf(int32_t k) { return k == K_INF || k == K_LLM; }
+
+// ---- serial helpers (thread 0 only) ------------------------------------------------
+
+__device__ void list_append(View& v, int32_t f, int32_t s) {
+  v.iNext[s] = -1;
+  if (v.fLt[f] < 0) v.fLh[f] = s; else v.iNext[v.fLt[f]] = s;
+  v.fLt[f] = s;
+}
+__device__ void list_remove(View& v, int32_t f, int32_t s) {
+  int32_t prev = -1, cur = v.fLh[f];
+  while (cur >= 0 && cur != s) { prev = cur; cur = v.iNext[cur]; }
+  if (cur < 0) return;
+  int32_t nx = v.iNext[cur];
+  if (prev < 0) v.fLh[f] = nx; else v.iNext[prev] = nx;
+  if (v.fLt[f] == s) v.fLt[f] = prev;
+}
+
+// resident order key: (prio, id) -- SLO-sensitive first (Alg.2)
+__device__ __forceinline__ long long res_key(const View& v, int32_t s) {
+  return ((long long)v.fPrio[v.iFunc[s]] << 32) | (uint32_t)v.iId[s];
+}
+
+__device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
+  View& v = c.v;
+  const int32_t f = v.iFunc[s];
+  if (v.gN[g] == 0) v.h[H_NACT] += 1;
+  v.gR[g] += v.fReq[f];
+  v.gL[g] += v.fLim[f];
+  v.gU[g] += share;
+  v.h[H_SUMU] += share;
+  int32_t* res = v.gRes + (size_t)g * RES;
+  int pos = v.gN[g];
+  const long long k = res_key(v, s);
+  while (pos > 0 && res_key(v, res[pos - 1]) > k) { res[pos] = res[pos - 1]; --pos; }
+  res[pos] = s;
+  v.gN[g] += 1;
+  const int32_t meta = v.iMeta[s];
+  const int k0 = nst_of(meta);
+  v.iG[s * MAXST + k0] = g;
+  v.iShare[s * MAXST + k0] = share;
+  v.iMeta[s] = (meta & ~(7 << 4)) | ((k0 + 1) << 4);
+  v.gExcl[g] = 1;             // I* of the request in flight (Q7)
+  v.h[H_DIRTY] = 1;
+}
+
+__device__ void release(Scn& c, int32_t s) {
+  View& v = c.v;
+  const int32_t f = v.iFunc[s];
+  const int32_t meta = v.iMeta[s];
+  const int n = nst_of(meta);
+  for (int k = 0; k < n; ++k) {
+    const int32_t g = v.iG[s * MAXST + k];
+    const int32_t sh = v.iShare[s * MAXST + k];
+    v.gR[g] -= v.fReq[f];
+    v.gL[g] -= v.fLim[f];
+    v.gU[g] -= sh;
+    v.h[H_SUMU] -= sh;
+    int32_t* res = v.gRes + (size_t)g * RES;
+    int j = 0;
+    const int nr = v.gN[g];
+    while (j < nr && res[j] != s) ++j;
+    for (; j + 1 < nr; ++j) res[j] = res[j + 1];
+    v.gN[g] = nr - 1;
+    if (nr - 1 == 0) v.h[H_NACT] -= 1;
+    v.iG[s * MAXST + k] = -1;
+    v.iShare[s * MAXST + k] = 0;
+  }
+  v.iMeta[s] = meta & ~(7 << 4);
+  v.h[H_DIRTY] = 1;
+}
+
+// terminate a live instance (placed or pending); frees its slot
+__device__ void terminate(Scn& c, int32_t s) {
+  View& v = c.v;
+  const int32_t f = v.iFunc[s];
+  if (st_of(v.iMeta[s]) == ST_PLACED) {
+    const int32_t ep = ++v.h[H_EPOCH];   // room was freed: queued failures may now succeed
+    const int ns = nst_of(v.iMeta[s]);
+    for (int k = 0; k < ns; ++k) {
+      const int32_t g = v.iG[s * MAXST + k];
+      v.gRel[g] = ep;
+      const int32_t slot = v.h[H_RLN]++ % RLOG;
+      v.rlG[slot] = g;
+      v.rlE[slot] = ep;
+    }
+    release(c, s);
+  }
+  v.iMeta[s] = ST_FREE;
+  list_remove(v, f, s);
+  v.fNlive[f] -= 1;
+  v.h[H_NLIVE] -= 1;
+  v.fstack[v.h[H_FSTOP]++] = s;
+}
+
+__device__ void compact_queue(View& v) {
+  const int32_t n = v.h[H_QLEN];
+  int32_t k = 0;
+  for (int32_t q = 0; q < n; ++q) {
+    if (v.qN[q] == 0) continue;
+    if (k != q) {
+      v.qFunc[k] = v.qFunc[q]; v.qFirst[k] = v.qFirst[q]; v.qN[k] = v.qN[q]; v.qFail[k] = v.qFail[q];
+    }
+    ++k;
+  }
+  v.h[H_QLEN] = k;
+}
+
+// enqueue one request of n new instances of f; returns first id or -1 on capacity error
+__device__ int32_t enqueue(Scn& c, int32_t f, int32_t n) {
+  View& v = c.v;
+  if (v.h[H_FSTOP] < n) { v.h[H_ERR] = 6; return -1; }
+  if (v.h[H_QLEN] == c.P->I) compact_queue(v);
+  const int32_t first = v.h[H_NEXT_IID];
+  for (int32_t j = 0; j < n; ++j) {
+    const int32_t s = v.fstack[--v.h[H_FSTOP]];
+    v.iId[s] = v.h[H_NEXT_IID]++;
+    v.iFunc[s] = f;
+    v.iMeta[s] = ST_PEND;
+    v.iReady[s] = 0;
+    for (int k = 0; k < MAXST; ++k) { v.iG[s * MAXST + k] = -1; v.iShare[s * MAXST + k] = 0; }
+    v.iBmin[s] = BIG;
+    v.iBmin[c.P->I + s] = BIG;
+    list_append(v, f, s);
+    v.fNlive[f] += 1;
+    v.h[H_NLIVE] += 1;
+  }
+  const int32_t q = v.h[H_QLEN]++;
+  v.qFunc[q] = f; v.qFirst[q] = first; v.qN[q] = n; v.qFail[q] = -1;
+  return first;
+}
+
+__device__ void register_func(View& v, int32_t f, int32_t t, int32_t Tp) {
+  if (v.fReg[f]) return;
+  v.fReg[f] = 1;
+  v.fNsamp[f] = 0; v.fAcc[f] = 0; v.fHead[f] = 0; v.fUp[f] = 0; v.fDown[f] = 0;
+  v.fThrn[f] = -1;
+  v.fPidx[f] = (int32_t)(((long long)t + v.fPhase[f]) % Tp);   // arrivals index for slot t
+}
+
+__device__ void kill_queue_entries_of(View& v, int32_t f) {
+  const int32_t n = v.h[H_QLEN];
+  for (int32_t q = 0; q < n; ++q) if (v.qN[q] > 0 && v.qFunc[q] == f) v.qN[q] = 0;
+}
+
+__device__ void kill_queue_entry_with_id(View& v, int32_t id) {
+  const int32_t n = v.h[H_QLEN];
+  for (int32_t q = 0; q < n; ++q)
+    if (v.qN[q] > 0 && v.qFirst[q] <= id && id < v.qFirst[q] + v.qN[q]) { v.qN[q] = 0; return; }
+}
+
+// ---- placement (collective) --------------------------------------------------------
+
+// Algorithm 1 for one instance s with Principle 2's LLM split before a new
+// GPU (Q11).  All threads call; thread 0 commits.  Returns a uniform success flag.
+__device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
+  View& v = c.v;
+  const Params& P = *c.P;
+  const int32_t f = v.iFunc[s];
+  const int32_t req = v.fReq[f], lim = v.fLim[f], mem = v.fMem[f], cls = v.fCls[f];
+  const long long aM = (long long)P.aw * P.M, bQ = (long long)P.bw * P.Q;
+  const unsigned long long MASK40 = (1ull << 40) - 1;
+  unsigned long long best = ~0ull;
+  for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
+    if (v.gExcl[g]) continue;
+    const int32_t n = v.gN[g];
+    unsigned long long key;
+    if (n == 0) {
+      key = (2ull << 62) | (MASK40 << 22) | (unsigned long long)g;  // tier 2, K := 0
+    } else {
+      const int32_t R = v.gR[g] + req, Lm = v.gL[g] + lim, U = v.gU[g] + mem;
+      if (!(R <= c.om && Lm <= c.ga && U <= P.M && n < RES)) continue;
+      const int32_t* res = v.gRes + (size_t)g * RES;
+      int aff = 0;
+      for (int j = 0; j < n && !aff; ++j) aff = (v.fCls[v.iFunc[res[j]]] == cls);
+      const unsigned long long K = (unsigned long long)(aM * R + bQ * U);
+      key = ((unsigned long long)(aff ? 0 : 1) << 62) | ((MASK40 - K) << 22) |
+            (unsigned long long)g;
+    }
+    best = key < best ? key : best;
+  }
+  best = block_min_u64(best, red, ph);
+  const int tier = best == ~0ull ? 3 : (int)(best >> 62);
+  if (tier <= 1) {
+    if (threadIdx.x == 0) commit(c, s, (int32_t)(best & 0x3FFFFF), mem);
+    __syncthreads();
+    return true;
+  }
+  if (v.fKind[f] == K_LLM && (P.flags & 1)) {
+    // worst-fit split: repeated argmax of free memory over active, cap-feasible GPUs
+    int32_t picked[MAXST];
+    int32_t pfree[MAXST];
+    int k = 0;
+    long long sum = 0;
+    bool okk = false;
+    for (int r = 0; r < P.max_stages; ++r) {
+      unsigned long long kk = ~0ull;
+      for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
+        const int32_t n = v.gN[g];
+        if (n == 0 || v.gExcl[g] || n >= RES) continue;
+        bool dup = false;
+        for (int j = 0; j < r; ++j) dup |= (picked[j] == g);
+        if (dup) continue;
+        if (v.gR[g] + req > c.om || v.gL[g] + lim > c.ga) continue;
+        const int32_t fr = P.M - v.gU[g];
+        if (fr <= 0) continue;
+        const unsigned long long key =
+            ((unsigned long long)(0xFFFFFFFFu - (uint32_t)fr) << 32) | (uint32_t)g;
+        kk = key < kk ? key : kk;
+      }
+      kk = block_min_u64(kk, red, ph);
+      if (kk == ~0ull) break;
+      picked[r] = (int32_t)(kk & 0xFFFFFFFFu);
+      pfree[r] = (int32_t)(0xFFFFFFFFu - (uint32_t)(kk >> 32));
+      sum += pfree[r];
+      k = r + 1;
+      if (sum >= mem) { okk = true; break; }
+    }
+    if (okk) {
+      if (threadIdx.x == 0) {
+        int32_t left = mem;
+        for (int j = 0; j < k; ++j) {
+          const int32_t sh = pfree[j] < left ? pfree[j] : left;
+          commit(c, s, picked[j], sh);
+          left -= sh;
+        }
+      }
+      __syncthreads();
+      return true;
+    }
+  }
+  if (tier == 2) {
+    if (threadIdx.x == 0) commit(c, s, (int32_t)(best & 0x3FFFFF), mem);
+    __syncthreads();
+    return true;
+  }
+  return false;
+}
+
+// Can GPU g, released after a request of f last failed, now change that outcome?
+// Non-LLM: g hosts one instance now (an emptied GPU always can).  LLM with split
+// enabled: g is also a split candidate (caps hold, some free memory).
+__device__ __forceinline__ bool could_help(const Scn& c, int32_t g, int32_t f) {
+  const View& v = c.v;
+  const Params& P = *c.P;
+  const int32_t n = v.gN[g];
+  if (n == 0) return true;
+  if (n >= RES || v.gR[g] + v.fReq[f] > c.om || v.gL[g] + v.fLim[f] > c.ga) return false;
+  if (v.gU[g] + v.fMem[f] <= P.M) return true;
+  return v.fKind[f] == K_LLM && (P.flags & 1) && P.M - v.gU[g] > 0;
+}
+
+// Could any GPU released after epoch fe now host a request of f?  Walks the release
+// log back to fe (usually 1-3 entries); falls back to scanning every GPU's last-release
+// epoch when the log no longer covers fe.
+__device__ bool hope_after(const Scn& c, int32_t fe, int32_t f) {
+  const View& v = c.v;
+  const int32_t n = v.h[H_RLN];
+  const int32_t lo = n > RLOG ? n - RLOG : 0;
+  if (n > RLOG && v.rlE[lo % RLOG] > fe) {
+    for (int32_t g = 0; g < c.P->G; ++g)
+      if (v.gRel[g] > fe && could_help(c, g, f)) return true;
+    return false;
+  }
+  for (int32_t k = n - 1; k >= lo; --k) {
+    if (v.rlE[k % RLOG] <= fe) break;
+    if (could_help(c, v.rlG[k % RLOG], f)) return true;
+  }
+  return false;
+}
+
+// Warp 0 walks the queue from position q, 32 entries per step (lane per entry):
+// requests that fail again by the skip rule are counted and stamped with the current
+// epoch; returns the first entry that needs a real attempt, or qn.  Lane 0 is thread 0
+// (owner of the thread-0 tallies).
+__device__ int32_t next_attempt(Scn& c, int32_t q, int32_t qn, Acc& acc) {
+  View& v = c.v;
+  const int lane = threadIdx.x & 31;
+  const int32_t ep = v.h[H_EPOCH];
+  int32_t nfail = 0, found = qn, nhope = 0;
+  for (int32_t p = q; p < qn; p += 32) {
+    const int32_t qq = p + lane;
+    int cls = 0;                      // 0 dead/none, 1 fails again, 2 needs an attempt
+    bool stamp = false;
+    if (qq < qn && v.qN[qq] > 0) {
+      const int32_t fe = v.qFail[qq];
+      if (fe < 0) cls = 2;                       // never tried
+      else if (fe == ep) cls = 1;                // nothing released since its failure
+      else {
+        ++nhope;
+        cls = hope_after(c, fe, v.qFunc[qq]) ? 2 : 1;
+        stamp = cls == 1;
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, cls == 2);
+    const int first = m ? __ffs(m) - 1 : 32;
+    const bool before = lane < first;
+    nfail += __popc(__ballot_sync(0xffffffffu, cls == 1 && before));
+    if (stamp && before) v.qFail[qq] = ep;
+    if (m) { found = p + first; break; }
+  }
+  for (int o = 16; o > 0; o >>= 1) nhope += __shfl_xor_sync(0xffffffffu, nhope, o);
+  if (lane == 0) {
+    acc.z->pfail += nfail;
+    acc.z->st[S_HOPE] += nhope;
+    acc.z->st[S_SCAN] += 1;
+  }
+  return found;
+}
+
+// One FIFO pass over the queue (Q8, Q9).
+// Retry skip (exact): a request that failed at release epoch E saw every
+// GPU unable to host it (and no inactive GPU).  Afterwards, GPUs without a release only
+// fill up, so the request can succeed again only through a GPU g released after E that
+// could host it now (gang: the count of hosting GPUs only grows through such g; LLM:
+// the top-4 free memory only grows through such g).  If no such g exists it fails
+// again without rescoring, exactly as the oracle's full rescoring would.
+__device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
+  View& v = c.v;
+  const int32_t qn = v.h[H_QLEN];
+  bool removed = false;
+  int32_t q = 0;
+  for (;;) {
+    if (threadIdx.x < 32) {
+      const int32_t e = next_attempt(c, q, qn, acc);
+      if (threadIdx.x == 0) red.flag = e;
+    }
+    __syncthreads();
+    q = red.flag;
+    if (q >= qn) break;
+    const int32_t n = v.qN[q];
+    const int32_t f = v.qFunc[q], first = v.qFirst[q];
+    if (threadIdx.x == 0) {          // gang members, ascending id
+      int j = 0;
+      for (int32_t s = v.fLh[f]; s >= 0 && j < n; s = v.iNext[s]) {
+        const int32_t id = v.iId[s];
+        if (id >= first && id < first + n) red.members[j++] = s;
+      }
+    }
+    __syncthreads();
+    int placed = 0;
+    if (threadIdx.x == 0) acc.z->st[S_ATTEMPT] += 1;
+    for (int j = 0; j < n; ++j) {
+      if (!place_one(c, red, ph, red.members[j])) break;
+      ++placed;
+    }
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < placed; ++j) {   // clear I* marks
+        const int32_t s = red.members[j];
+        const int ns = nst_of(v.iMeta[s]);
+        for (int k = 0; k < ns; ++k) v.gExcl[v.iG[s * MAXST + k]] = 0;
+      }
+      if (placed == n) {
+        const int32_t cold = v.fCold[f];
+        for (int j = 0; j < n; ++j) {
+          const int32_t s = red.members[j];
+          v.iMeta[s] = (v.iMeta[s] & ~3) | ST_PLACED;
+          v.iReady[s] = t + cold;
+          acc.z->pok += 1;
+          if (is_inf(v.fKind[f]) && cold > 0) acc.z->cold += 1;
+          if (nst_of(v.iMeta[s]) > 1) acc.z->split += 1;
+        }
+        v.qN[q] = 0;
+        removed = true;
+      } else {
+        for (int j = 0; j < placed; ++j) release(c, red.members[j]);  // rollback
+        acc.z->pfail += 1;
+        v.qFail[q] = v.h[H_EPOCH];
+      }
+    }
+    __syncthreads();
+    ++q;
+  }
+  if (threadIdx.x == 0 && removed) compact_queue(v);
+}
+
+// ---- B5: pack GPU rows into 32-lane warp chunks by width class (1..32 lanes) ----------
+
+__device__ __forceinline__ int width_class(int32_t n) {
+  return n <= 1 ? 0 : 32 - __clz(n - 1);
+}
+
+__device__ void rebuild_layout(Scn& c) {
+  View& v = c.v;
+  const Params& P = *c.P;
+  if (threadIdx.x < 6) { v.h[H_CCNT + threadIdx.x] = 0; v.h[H_CCNT2 + threadIdx.x] = 0; }
+  __syncthreads();
+  for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
+    const int32_t n = v.gN[g];
+    if (n > 0) atomicAdd(&v.h[H_CCNT + width_class(n)], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t cb = 0, gb = 0;
+    for (int k = 0; k < 6; ++k) {
+      v.h[H_CBASE + k] = cb;
+      v.h[H_GBASE + k] = gb;
+      const int32_t per = 32 >> k;
+      cb += (v.h[H_CCNT + k] + per - 1) / per;
+      gb += v.h[H_CCNT + k];
+    }
+    v.h[H_CBASE + 6] = cb;
+    v.h[H_DIRTY] = 0;
+  }
+  __syncthreads();
+  for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
+    const int32_t n = v.gN[g];
+    if (n > 0) {
+      const int k = width_class(n);
+      const int32_t idx = atomicAdd(&v.h[H_CCNT2 + k], 1);
+      v.gGrow[v.h[H_GBASE + k] + idx] = g;   // order inside a class is irrelevant
+    }
+  }
+  __syncthreads();
+}
+
+// ---- per-slot phases ------------------------------------------------------------------
+
+
+// P0: arrivals and even dispatch over warm instances (Q16, Q17).
+// A_f(t) = (pat[p_f][(t + phase_f) mod T_pat] * scale_f) >> 10; the pattern index is
+// advanced incrementally (set at registration), so no modulo runs per slot.
+__device__ void phase0(Scn& c, int32_t t, Acc& acc) {
+  View& v = c.v;
+  const Params& P = *c.P;
+  const int32_t* __restrict__ infl = v.fInfL;
+  const int32_t* __restrict__ reg = v.fReg;
+  const int32_t* __restrict__ fpat = v.fPat;
+  const int32_t* __restrict__ fscale = v.fScale;
+  int32_t* __restrict__ pidx = v.fPidx;
+  int32_t* __restrict__ facc = v.fAcc;
+  const int32_t* __restrict__ lh = v.fLh;
+  const int32_t* __restrict__ nxt = v.iNext;
+  const int32_t* __restrict__ meta = v.iMeta;
+  const int32_t* __restrict__ ready = v.iReady;
+  int32_t* __restrict__ r = v.iR + (t & 1) * P.I;
+  const int32_t* __restrict__ gpat = P.pat;
+  const int32_t Tp = P.Tp, ninf = v.h[H_NINF];
+  for (int32_t k = threadIdx.x; k < ninf; k += blockDim.x) {
+    const int32_t f = infl[k];
+    if (!reg[f]) continue;
+    const int32_t idx = pidx[f];
+    pidx[f] = idx + 1 == Tp ? 0 : idx + 1;
+    const long long x = __ldg(gpat + (size_t)fpat[f] * Tp + idx);
+    const int32_t A = (int32_t)((x * fscale[f]) >> 10);
+    facc[f] += A;
+    acc.rtot += A;
+    int32_t nw = 0;
+    for (int32_t s = lh[f]; s >= 0; s = nxt[s])
+      nw += (st_of(meta[s]) == ST_PLACED && ready[s] <= t);
+    if (nw == 0) { acc.rvio += A; continue; }
+    const int32_t q = A / nw, rem = A - q * nw;
+    int32_t rank = 0;
+    for (int32_t s = lh[f]; s >= 0; s = nxt[s]) {
+      if (st_of(meta[s]) == ST_PLACED && ready[s] <= t) {
+        r[s] = q + (rank < rem ? 1 : 0);
+        ++rank;
+      }
+    }
+  }
+}
+
+// P1: vertical token allocation per GPU row (Q13, Q14)
+__device__ void phase1(Scn& c, int32_t t, Acc& acc) {
+  View& v = c.v;
+  const Params& P = *c.P;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int par = t & 1;
+  const int32_t* __restrict__ r = v.iR + par * P.I;
+  int32_t* bmin = v.iBmin + par * P.I;
+  int32_t* gang = v.fGang + par * P.F;
+  const int32_t* __restrict__ grow = v.gGrow;
+  const int32_t* __restrict__ gn = v.gN;
+  const int32_t* __restrict__ gres = v.gRes;
+  const int32_t* __restrict__ meta_ = v.iMeta;
+  const int32_t* __restrict__ ready = v.iReady;
+  const int32_t* __restrict__ ifunc = v.iFunc;
+  const int32_t* __restrict__ iid = v.iId;
+  const int32_t* __restrict__ fkind = v.fKind;
+  const int32_t* __restrict__ freq = v.fReq;
+  const int32_t* __restrict__ flim = v.fLim;
+  const int32_t* __restrict__ fdtr = v.fDtr;
+  const int32_t* __restrict__ fibs = v.fIbs;
+  const int32_t* __restrict__ fcb = v.fCb;
+  const int32_t* __restrict__ cbase = v.h + H_CBASE;
+  const int32_t* __restrict__ ccnt = v.h + H_CCNT;
+  const int32_t* __restrict__ gbase = v.h + H_GBASE;
+  const int32_t nch = cbase[6];
+  const int32_t T = (int32_t)P.T_slot, slot_ms = P.slot_ms;
+  const uint64_t ht = sm64(sm64((uint32_t)c.scn_id) ^ (uint32_t)t);   // mix() prefix, per slot
+  for (int32_t ch = wid; ch < nch; ch += nwarp) {
+    int k = 0;
+#pragma unroll
+    for (int x = 1; x < 6; ++x) k += (ch >= cbase[x]);
+    const int w = 1 << k;
+    const int32_t gi = (ch - cbase[k]) * (32 >> k) + (lane >> k);
+    int32_t g = -1, s = -1;
+    if (gi < ccnt[k]) {
+      g = grow[gbase[k] + gi];
+      const int j = lane & (w - 1);
+      if (j < gn[g]) s = gres[(size_t)g * RES + j];
+    }
+    int32_t req = 0, want = 0, f = -1, kind = 0, nst = 1, cst = 1, ibs = 1, rr = 0, need = 0;
+    int32_t d = 0;
+    bool warm = false;
+    if (s >= 0) {
+      const int32_t meta = meta_[s];
+      warm = st_of(meta) == ST_PLACED && ready[s] <= t;
+      if (warm) {
+        f = ifunc[s];
+        kind = fkind[f];
+        nst = nst_of(meta);
+        req = freq[f] * slot_ms;
+        const int32_t lim = flim[f] * slot_ms;
+        long long dd;
+        if (kind == K_TRAIN) {
+          dd = fdtr[f];
+        } else {
+          ibs = fibs[f];
+          const int32_t cb = fcb[f];
+          cst = nst == 1 ? cb : (cb + nst - 1) / nst;   // c_stage (R4)
+          rr = r[s];
+          need = rr / ibs + (rr % ibs != 0);             // ceil(r / IBS) batches
+          dd = (long long)need * cst;
+        }
+        d = dd < lim ? (int32_t)dd : lim;                // min(d, limit) (want only uses this)
+        want = d > req ? d - req : 0;
+        if (kind == K_TRAIN) d = (int32_t)dd;            // training keeps x = min(d, a)
+      }
+    }
+    // width-w segmented inclusive scan of want, and row sum of req
+    int32_t incl = want, sreq = req;
+    for (int o = 1; o < w; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, incl, o, w);
+      if ((lane & (w - 1)) >= o) incl += y;
+    }
+    for (int o = w >> 1; o > 0; o >>= 1) sreq += __shfl_xor_sync(0xffffffffu, sreq, o, w);
+    if (warm) {
+      const int32_t room = T - sreq - (incl - want);
+      const int32_t sp = want < room ? want : (room > 0 ? room : 0);
+      const int32_t a = req + sp;
+      acc.hash += sm64(sm64(ht ^ (uint32_t)iid[s]) ^ ((uint64_t((uint32_t)g) << 32) | (uint32_t)a));
+      if (kind == K_TRAIN) {
+        atomicMin(&gang[f], d < a ? d : a);              // x = min(d, a)
+      } else {
+        const int32_t fit = a / cst;
+        const int32_t b = need < fit ? need : fit;
+        if (nst == 1) {
+          const long long cap = (long long)b * ibs;
+          const int32_t served = cap < rr ? (int32_t)cap : rr;
+          acc.rsrv += served;
+          acc.rvio += rr - served;
+          const long long e = (long long)b * cst;
+          acc.iexe += e;
+          acc.etot += e;
+        } else {
+          atomicMin(&bmin[s], b);
+        }
+      }
+    }
+  }
+}
+
+// P2: cross-row minima -- training gang (Q22) and LLM pipeline stages (Q11); only the
+// training and LLM functions (static list fDefL) are visited.
+__device__ void phase2(Scn& c, int32_t t, Acc& acc) {
+  View& v = c.v;
+  const Params& P = *c.P;
+  const int par = t & 1;
+  const int32_t* __restrict__ r = v.iR + par * P.I;
+  int32_t* bmin = v.iBmin + par * P.I;
+  int32_t* gang = v.fGang + par * P.F;
+  const int32_t* __restrict__ defl = v.fDefL;
+  const int32_t* __restrict__ reg = v.fReg;
+  const int32_t* __restrict__ lh = v.fLh;
+  const int32_t* __restrict__ nxt = v.iNext;
+  const int32_t* __restrict__ meta = v.iMeta;
+  const int32_t ndef = v.h[H_NDEF];
+  for (int32_t k = threadIdx.x; k < ndef; k += blockDim.x) {
+    const int32_t f = defl[k];
+    if (!reg[f]) continue;
+    if (v.fKind[f] == K_TRAIN) {
+      // the job is the function: gang = min x over its live workers, 0 unless all are
+      // warm; every warm worker executes the gang, progress = n_workers * gang (Q22)
+      const int32_t gm = gang[f];
+      if (gm != BIG) {
+        gang[f] = BIG;
+        int32_t nlive = 0;
+        bool all_warm = true;
+        for (int32_t s = lh[f]; s >= 0; s = nxt[s]) {
+          ++nlive;
+          all_warm &= st_of(meta[s]) == ST_PLACED && v.iReady[s] <= t;
+        }
+        if (all_warm) {
+          acc.tprg += (long long)v.fNw[f] * gm;
+          acc.etot += (long long)nlive * gm;
+        }
+      }
+    } else {
+      for (int32_t s = lh[f]; s >= 0; s = nxt[s]) {
+        const int32_t b = bmin[s];
+        if (b == BIG) continue;
+        bmin[s] = BIG;
+        const int32_t nst = nst_of(meta[s]);
+        const int32_t ibs = v.fIbs[f];
+        const int32_t cst = (v.fCb[f] + nst - 1) / nst;
+        const int32_t rr = r[s];
+        const long long cap = (long long)b * ibs;
+        const int32_t served = cap < rr ? (int32_t)cap : rr;
+        acc.rsrv += served;
+        acc.rvio += rr - served;
+        const long long e = (long long)nst * b * cst;
+        acc.iexe += e;
+        acc.etot += e;
+      }
+    }
+  }
+}
+
+// ---- boundary -----------------------------------------------------------------------
+
+enum : int32_t { EV_DEP = 1, EV_OUT = 2, EV_IN = 4, EV_ARR = 8 };
+
+__device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
+  View& v = c.v;
+  const Params& P = *c.P;
+  const int32_t sec = t / P.SPS;
+  // B1 (function-parallel): window push, incremental counts, decisions, event flags.
+  // Contiguous function ranges per thread keep the event list in ascending order.
+  const int32_t* __restrict__ fkind = v.fKind;
+  int32_t* __restrict__ reg = v.fReg;
+  const int32_t* __restrict__ farr = v.fArr;
+  const int32_t* __restrict__ fdep = v.fDep;
+  const long long* __restrict__ fcap1 = reinterpret_cast<const long long*>(v.fCap1);
+  int32_t* __restrict__ facc = v.fAcc;
+  int32_t* __restrict__ fhead = v.fHead;
+  int32_t* __restrict__ fns = v.fNsamp;
+  int32_t* __restrict__ fthr = v.fThrn;
+  int32_t* __restrict__ fup = v.fUp;
+  int32_t* __restrict__ fdown = v.fDown;
+  const int32_t* __restrict__ fnlive = v.fNlive;
+  int32_t* __restrict__ fflag = v.fFlag;
+  int32_t* __restrict__ ringb = v.ring;
+  const int32_t W = P.W;
+  const int32_t per = (P.F + blockDim.x - 1) / blockDim.x;
+  const int32_t lo = threadIdx.x * per, hi = min(P.F, lo + per);
+  int32_t cnt = 0;
+  for (int32_t f = lo; f < hi; ++f) {
+    const int32_t kind = fkind[f];
+    int32_t ev = 0;
+    if (kind != K_UNUSED) {
+      if (reg[f]) {
+        const bool inf = is_inf(kind);
+        int32_t* ring = ringb + (size_t)f * W;
+        const long long cap1 = fcap1[f];
+        if (inf && sec >= 1) {                      // step 1: push second sec-1
+          const int32_t val = facc[f];
+          const int32_t head = fhead[f];
+          const int32_t ns = fns[f];
+          const int32_t thr = fthr[f];
+          if (thr >= 0) {
+            const long long cu = (long long)thr * cap1, cd = (long long)(thr - 1) * cap1;
+            int32_t du = val > cu, dd = val < cd;
+            if (ns >= W) { const int32_t old = ring[head]; du -= old > cu; dd -= old < cd; }
+            fup[f] += du;
+            fdown[f] += dd;
+          }
+          ring[head] = val;
+          fhead[f] = head + 1 == W ? 0 : head + 1;
+          fns[f] = ns + 1;
+          facc[f] = 0;
+        }
+        if (fdep[f] == sec) {                       // step 2: departure
+          ev = EV_DEP;
+        } else if (inf && fns[f] >= W) {            // step 3: lazy scaling decision
+          const int32_t n = fnlive[f];
+          const long long cu = (long long)n * cap1, cd = (long long)(n - 1) * cap1;
+          if (fthr[f] != n) {
+            int32_t up = 0, dn = 0;
+            for (int j = 0; j < W; ++j) { const int32_t w = ring[j]; up += w > cu; dn += w < cd; }
+            fup[f] = up; fdown[f] = dn; fthr[f] = n;
+          }
+          if (fup[f] >= P.phi_out) {
+            int32_t mx = 0;
+            for (int j = 0; j < W; ++j) mx = max(mx, ring[j]);
+            const long long k = ((long long)mx + cap1 - 1) / cap1 - n;
+            if (k >= 1) { ev = EV_OUT; v.fK[f] = (int32_t)k; }
+          } else if (fdown[f] > P.phi_in && n > P.min_inst) {
+            ev = EV_IN;
+          }
+        }
+      }
+      if (farr[f] == sec) ev |= EV_ARR;             // step 4: arrival
+    }
+    fflag[f] = ev;
+    cnt += ev != 0;
+  }
+  const int32_t any = __syncthreads_count(cnt);
+  int32_t total = 0;
+  if (any) {                                        // ordered compaction of the events
+    int32_t pos = block_scan_i32(cnt, red, ph, &total);
+    for (int32_t f = lo; f < hi && cnt; ++f)
+      if (fflag[f]) { v.fList[pos++] = f; --cnt; }
+  }
+  const int32_t need_pass = total > 0 || v.h[H_QLEN] > 0;
+  __syncthreads();
+  if (!need_pass) return;
+  // B3: apply in the paper's order (steps 2, 3, 4), thread 0
+  if (threadIdx.x == 0 && total > 0) {
+    acc.z->st[S_EVENT] += total;
+    for (int32_t e = 0; e < total; ++e) {     // step 2: departures
+      const int32_t f = v.fList[e];
+      if (!(v.fFlag[f] & EV_DEP)) continue;
+      kill_queue_entries_of(v, f);
+      while (v.fLh[f] >= 0) terminate(c, v.fLh[f]);
+      v.fReg[f] = 0;
+    }
+    for (int32_t e = 0; e < total && !v.h[H_ERR]; ++e) {     // step 3: hscaler actions
+      const int32_t f = v.fList[e];
+      const int32_t ev = v.fFlag[f];
+      if (ev & EV_OUT) {
+        for (int32_t j = 0; j < v.fK[f] && !v.h[H_ERR]; ++j) enqueue(c, f, 1);
+        acc.z->sout += 1;
+      } else if (ev & EV_IN) {
+        const int32_t victim = v.fLt[f];        // highest live id (Q19)
+        if (st_of(v.iMeta[victim]) == ST_PEND) kill_queue_entry_with_id(v, v.iId[victim]);
+        terminate(c, victim);
+        acc.z->sin += 1;
+      }
+    }
+    for (int32_t e = 0; e < total && !v.h[H_ERR]; ++e) {     // step 4: arrivals
+      const int32_t f = v.fList[e];
+      if (!(v.fFlag[f] & EV_ARR)) continue;
+      register_func(v, f, t, P.Tp);
+      if (v.fKind[f] == K_TRAIN) enqueue(c, f, v.fNw[f]);
+      else for (int32_t j = 0; j < P.min_inst && !v.h[H_ERR]; ++j) enqueue(c, f, 1);
+    }
+  }
+  __syncthreads();
+  if (v.h[H_ERR]) return;
+  placement_pass(c, red, ph, t, acc);             // step 5
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------- kernels
+
+// One scenario for one call (scale_step: n_req < 0; place_batch: n_req >= 0).
+template <bool SMEM>
+__device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem, int32_t sc, int32_t t0,
+                             int32_t n_slots, int32_t n_req, const int32_t* req_scn,
+                             const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid) {
+  uint8_t* gblock = P.state + (size_t)sc * P.L.bytes;
+  uint8_t* hot = gblock;
+  if (SMEM) {
+    const int4* src = reinterpret_cast<const int4*>(gblock);
+    int4* dst = reinterpret_cast<int4*>(smem);
+    for (size_t k = threadIdx.x; k < P.L.hot_bytes / 16; k += blockDim.x) dst[k] = src[k];
+    hot = smem;
+  }
+  if (threadIdx.x == 0) {
+    sv = make_view(hot, gblock, P.L);
+    sv.ring = P.ring + (size_t)sc * P.F * P.W;
+  }
+  Scn c{sv};
+  c.P = &P;
+  c.frow = P.funcs + (size_t)sc * P.F * 16;
+  c.scn_id = P.scen[sc * 4 + 0];
+  c.om = P.scen[sc * 4 + 1];
+  c.ga = P.scen[sc * 4 + 2];
+  Acc acc = {};
+  acc.z = &red.z;
+  if (threadIdx.x == 0) red.z = Acc0{};
+  int ph = 0;
+  View& v = c.v;
+  __syncthreads();
+  if (v.h[H_ERR]) return;
+
+  if (n_req >= 0) {
+    // ---- dilu_place_batch: enqueue this scenario's requests in array order, one pass
+    if (threadIdx.x == 0) {
+      for (int32_t j = 0; j < n_req && !v.h[H_ERR]; ++j) {
+        if (req_scn[j] != sc) continue;
+        const int32_t f = req_func[j];
+        register_func(v, f, t0, P.Tp);
+        out_iid[j] = enqueue(c, f, v.fKind[f] == K_TRAIN ? v.fNw[f] : 1);
+      }
+    }
+    __syncthreads();
+    if (!v.h[H_ERR]) placement_pass(c, red, ph, t0, acc);
+    __syncthreads();
+    for (int32_t j = threadIdx.x; j < n_req; j += blockDim.x) {
+      if (req_scn[j] != sc) continue;
+      const int32_t id = out_iid[j];
+      int32_t g = -1;
+      for (int32_t s = v.fLh[req_func[j]]; s >= 0; s = v.iNext[s])
+        if (v.iId[s] == id) { if (st_of(v.iMeta[s]) == ST_PLACED) g = v.iG[s * MAXST]; break; }
+      out_gpu[j] = g;
+    }
+  } else {
+    // ---- dilu_scale_step: the slot loop
+    for (int32_t t = t0; t < t0 + n_slots; ++t) {
+      if (t % P.SPS == 0) {
+        __syncthreads();                    // P2(t-1) done before state mutates
+        boundary(c, red, ph, t, acc);
+        if (v.h[H_ERR]) break;
+      }
+      if (v.h[H_DIRTY]) {
+        __syncthreads();
+        rebuild_layout(c);
+        if (threadIdx.x == 0) acc.z->st[S_LAYOUT] += 1;
+      }
+      phase0(c, t, acc);
+      if (threadIdx.x == 0) {
+        const long long na = v.h[H_NACT];
+        acc.z->act += na;
+        acc.z->memu += na * P.M - v.h[H_SUMU];
+        acc.z->rows += P.G;
+        acc.z->maxa = na > acc.z->maxa ? na : acc.z->maxa;
+        acc.z->st[S_SLOT] += 1;
+      }
+      __syncthreads();
+      phase1(c, t, acc);
+      __syncthreads();
+      phase2(c, t, acc);
+    }
+  }
+  __syncthreads();
+
+  // ---- block-reduce the tallies once per call
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    long long vals[7] = {acc.rtot, acc.rsrv, acc.rvio, acc.iexe, acc.tprg, acc.etot,
+                         (long long)acc.hash};
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      long long x = vals[q];
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) red.acc[q][wid] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long s7[7] = {0, 0, 0, 0, 0, 0, 0};
+      for (int q = 0; q < 7; ++q)
+        for (int k = 0; k < nw; ++k)
+          s7[q] = (long long)((unsigned long long)s7[q] + (unsigned long long)red.acc[q][k]);
+      long long* T = reinterpret_cast<long long*>(P.tally) + (size_t)sc * NT;
+      T[T_ACT] += acc.z->act;
+      T[T_SMU] += acc.z->act * P.T_slot - s7[5];
+      T[T_MEMU] += acc.z->memu;
+      T[T_RTOT] += s7[0];
+      T[T_RSRV] += s7[1];
+      T[T_RVIO] += s7[2];
+      T[T_IEXE] += s7[3];
+      T[T_TPRG] += s7[4];
+      T[T_POK] += acc.z->pok;
+      T[T_PFAIL] += acc.z->pfail;
+      T[T_COLD] += acc.z->cold;
+      T[T_SOUT] += acc.z->sout;
+      T[T_SIN] += acc.z->sin;
+      T[T_SPLIT] += acc.z->split;
+      T[T_HASH] = (long long)((unsigned long long)T[T_HASH] + (unsigned long long)s7[6]);
+      T[T_ROWS] += acc.z->rows;
+      if (acc.z->maxa > T[T_MAXA]) T[T_MAXA] = acc.z->maxa;
+      long long* ST = reinterpret_cast<long long*>(P.stats) + (size_t)sc * NSTAT;
+      for (int k = 0; k < NSTAT; ++k) ST[k] += acc.z->st[k];
+    }
+  }
+  if (SMEM) {
+    __syncthreads();
+    const int4* src = reinterpret_cast<const int4*>(smem);
+    int4* dst = reinterpret_cast<int4*>(gblock);
+    for (size_t k = threadIdx.x; k < P.L.hot_bytes / 16; k += blockDim.x) dst[k] = src[k];
+  }
+  __syncthreads();
+}
+
+// Persistent CTAs: each pulls the next scenario from an atomic counter (zeroed by the
+// host before the launch), so long scenarios do not leave SMs idle at the tail.
+#ifndef DILU_MINB
+#define DILU_MINB 3
+#endif
+constexpr int SMEM_MAX_THREADS = 256;   // shared-memory variant: <=256 threads, DILU_MINB CTAs/SM
+
+template <bool SMEM>
+__global__ void __launch_bounds__(SMEM ? SMEM_MAX_THREADS : 1024, SMEM ? DILU_MINB : 1)
+k_run(Params Pin, int32_t* next_scn, int32_t t0,
+                                              int32_t n_slots, int32_t n_req,
+                                              const int32_t* req_scn, const int32_t* req_func,
+                                              int32_t* out_gpu, int32_t* out_iid) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ Red red;
+  __shared__ Params sP;
+  __shared__ View sv;
+  if (threadIdx.x == 0) sP = Pin;
+  for (;;) {
+    if (threadIdx.x == 0) red.flag = atomicAdd(next_scn, 1);
+    __syncthreads();
+    const int32_t sc = red.flag;
+    __syncthreads();
+    if (sc >= sP.S) break;
+    run_scenario<SMEM>(sP, red, sv, smem, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu, out_iid);
+  }
+}
+
+// Initialise every scenario's block at slot 0 (one CTA per scenario).
+__global__ void k_init(Params P) {
+  const int32_t sc = blockIdx.x;
+  uint8_t* b = P.state + (size_t)sc * P.L.bytes;
+  View v = make_view(b, b, P.L);
+  const int32_t* rows = P.funcs + (size_t)sc * P.F * 16;
+  for (int k = threadIdx.x; k < H_WORDS; k += blockDim.x) v.h[k] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) { v.h[H_FSTOP] = P.I; v.h[H_DIRTY] = 1; }
+  for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
+    v.gR[g] = 0; v.gL[g] = 0; v.gU[g] = 0; v.gN[g] = 0; v.gExcl[g] = 0; v.gGrow[g] = 0;
+    v.gRel[g] = 0;
+  }
+  for (int32_t k = threadIdx.x; k < P.G * RES; k += blockDim.x) v.gRes[k] = -1;
+  for (int32_t s = threadIdx.x; s < P.I; s += blockDim.x) {
+    v.iId[s] = -1; v.iFunc[s] = -1; v.iMeta[s] = ST_FREE; v.iReady[s] = 0; v.iNext[s] = -1;
+    for (int k = 0; k < MAXST; ++k) { v.iG[s * MAXST + k] = -1; v.iShare[s * MAXST + k] = 0; }
+    v.iR[s] = 0; v.iR[P.I + s] = 0; v.iBmin[s] = BIG; v.iBmin[P.I + s] = BIG;
+    v.fstack[s] = P.I - 1 - s;
+  }
+  for (int32_t f = threadIdx.x; f < P.F; f += blockDim.x) {
+    const int32_t* r = rows + (size_t)f * 16;
+    const int32_t kind = r[0];
+    v.fKind[f] = kind; v.fPrio[f] = r[1]; v.fIbs[f] = r[2] > 0 ? r[2] : 1; v.fReq[f] = r[3];
+    v.fLim[f] = r[4]; v.fMem[f] = r[5]; v.fCb[f] = r[6] > 0 ? r[6] : 1; v.fNw[f] = r[7];
+    v.fCold[f] = r[9]; v.fCls[f] = r[10]; v.fPat[f] = r[13]; v.fScale[f] = r[14];
+    v.fPhase[f] = r[15];
+    const long long lim_tok = (long long)r[4] * P.slot_ms;
+    v.fDtr[f] = kind == K_TRAIN ? (int32_t)(lim_tok * r[8] / 1000) : 0;
+    // R5: cap1 = (1000/slot_ms) * floor(req_tok / c_b) * IBS
+    v.fCap1[f] = is_inf(kind) ? (long long)P.SPS * (((long long)r[3] * P.slot_ms) / r[6]) * r[2] : 0;
+    v.fReg[f] = 0; v.fNsamp[f] = 0; v.fAcc[f] = 0; v.fHead[f] = 0; v.fUp[f] = 0; v.fDown[f] = 0;
+    v.fThrn[f] = -1; v.fNlive[f] = 0; v.fLh[f] = -1; v.fLt[f] = -1;
+    v.fGang[f] = BIG; v.fGang[P.F + f] = BIG; v.fFlag[f] = 0; v.fK[f] = 0; v.fList[f] = 0;
+    v.fArr[f] = r[11]; v.fDep[f] = r[12]; v.fPidx[f] = 0;
+  }
+  if (threadIdx.x == 0) {   // static lists: inference functions (P0), training + LLM (P2)
+    int32_t ni = 0, nd = 0;
+    for (int32_t f = 0; f < P.F; ++f) {
+      const int32_t kind = rows[(size_t)f * 16];
+      if (is_inf(kind)) v.fInfL[ni++] = f;
+      if (kind == K_TRAIN || kind == K_LLM) v.fDefL[nd++] = f;
+    }
+    v.h[H_NINF] = ni;
+    v.h[H_NDEF] = nd;
+  }
+  for (int32_t q = threadIdx.x; q < P.I; q += blockDim.x) {
+    v.qFunc[q] = 0; v.qFirst[q] = 0; v.qN[q] = 0; v.qFail[q] = -1;
+  }
+  for (int k = threadIdx.x; k < NT; k += blockDim.x) P.tally[(size_t)sc * NT + k] = 0;
+  for (int k = threadIdx.x; k < NSTAT; k += blockDim.x) P.stats[(size_t)sc * NSTAT + k] = 0;
+  for (int k = threadIdx.x; k < RLOG; k += blockDim.x) { v.rlG[k] = 0; v.rlE[k] = 0; }
+}
+
+// Snapshot for parity tests (off the timed path).
+__global__ void k_snapshot(Params P, int32_t id_cap, int32_t* out_gpu, int32_t* out_inst) {
+  const int32_t sc = blockIdx.x;
+  View v = make_view(P.state + (size_t)sc * P.L.bytes, P.state + (size_t)sc * P.L.bytes, P.L);
+  if (out_gpu)
+    for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
+      int32_t* o = out_gpu + ((size_t)sc * P.G + g) * 4;
+      o[0] = v.gR[g]; o[1] = v.gL[g]; o[2] = v.gU[g]; o[3] = v.gN[g];
+    }
+  if (!out_inst) return;
+  const int32_t issued = v.h[H_NEXT_IID];
+  for (int32_t id = threadIdx.x; id < id_cap; id += blockDim.x) {
+    int32_t* o = out_inst + ((size_t)sc * id_cap + id) * 12;
+    if (id >= issued) { for (int k = 0; k < 12; ++k) o[k] = -1; continue; }
+    // terminated unless a live slot overwrites it below
+    o[0] = -1; o[1] = 2; o[2] = 0; o[3] = -1;
+    for (int k = 0; k < MAXST; ++k) { o[4 + k] = -1; o[8 + k] = 0; }
+  }
+  __syncthreads();
+  for (int32_t s = threadIdx.x; s < P.I; s += blockDim.x) {
+    const int32_t meta = v.iMeta[s];
+    if (st_of(meta) == ST_FREE) continue;
+    const int32_t id = v.iId[s];
+    if (id >= id_cap) continue;
+    int32_t* o = out_inst + ((size_t)sc * id_cap + id) * 12;
+    const bool pl = st_of(meta) == ST_PLACED;
+    o[0] = v.iFunc[s];
+    o[1] = pl ? 1 : 0;
+    o[2] = pl ? nst_of(meta) : 0;
+    o[3] = pl ? v.iReady[s] : -1;
+    for (int k = 0; k < MAXST; ++k) {
+      const bool on = pl && k < nst_of(meta);
+      o[4 + k] = on ? v.iG[s * MAXST + k] : -1;
+      o[8 + k] = on ? v.iShare[s * MAXST + k] : 0;
+    }
+  }
+}
+
+}  // namespace dilu

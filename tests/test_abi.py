@@ -1,0 +1,70 @@
+"""CPU-side checks of the boundary: libdilu.so builds for sm_100a, loads, and exports
+every function include/dilu.h declares; the ABI struct sizes match the generator's
+field lists; the product package never imports the oracle."""
+import ast
+import os
+import re
+
+import pytest
+
+import dilu_inputs as di
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "dilu.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:[\w\s\*]+?)\b(dilu_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2503_05130_b200 import _build
+    import ctypes
+    path = _build.build()
+    L = ctypes.CDLL(path)
+    names = header_functions()
+    assert "dilu_sim_create" in names and "dilu_scale_step" in names
+    for n in names:
+        assert hasattr(L, n), n
+    import paper_2503_05130_b200 as pkg
+    assert sorted(pkg.EXPORTED) == names
+
+
+def test_struct_field_counts_match_header():
+    src = open(os.path.join(ROOT, "include", "dilu.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+
+    def fields(name):
+        body = re.search(r"typedef struct \{([^{}]*)\}\s*" + name + ";", src).group(1)
+        return sum(len(d.split(",")) for d in re.findall(r"int32_t\s+([^;]+);", body))
+    assert fields("dilu_config") == len(di.CONFIG_FIELDS)
+    assert fields("dilu_func") == len(di.FUNC_FIELDS)
+    assert fields("dilu_scenario") == len(di.SCEN_FIELDS)
+
+
+def test_workspace_bytes_and_validation_without_gpu():
+    import numpy as np
+    import paper_2503_05130_b200 as pkg
+    wl = di.c4(n_scenarios=8, T=100)
+    n = pkg.dilu_workspace_bytes(wl.cfg_array())
+    assert n > 0 and n % 256 == 0
+    bad = wl.cfg_array().copy()
+    bad[di.CONFIG_FIELDS.index("q_pm")] = 999
+    assert pkg.dilu_workspace_bytes(bad) == 0
+
+
+def test_product_package_does_not_touch_oracle():
+    pkg_dir = os.path.join(ROOT, "paper_2503_05130_b200")
+    for dp, _, files in os.walk(pkg_dir):
+        for fn in files:
+            p = os.path.join(dp, fn)
+            if fn.endswith(".py"):
+                tree = ast.parse(open(p).read())
+                for node in ast.walk(tree):
+                    if isinstance(node, ast.Import):
+                        assert all(not a.name.startswith("oracle") for a in node.names), p
+                    if isinstance(node, ast.ImportFrom):
+                        assert not (node.module or "").startswith("oracle"), p
+            if fn.endswith((".cu", ".cuh", ".h")):
+                assert "dilu_ref" not in open(p).read(), p

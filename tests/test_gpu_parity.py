@@ -1,0 +1,173 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by
+element on the same seeded inputs.  Integer tallies, the uint64 allocation hash,
+placements (GPU state + every instance's GPUs/shares/ready slot) must be bit-exact.
+Float ratios are derived on the host from identical integers (tol 1e-9 rel)."""
+import os
+
+import numpy as np
+import pytest
+
+import dilu_inputs as di
+import oracle
+
+pytestmark = pytest.mark.gpu
+T = {n: i for i, n in enumerate(di.TALLY_NAMES)}
+
+
+def gpu_sim(wl):
+    from paper_2503_05130_b200 import DiluSim
+    return DiluSim.from_workload(wl)
+
+
+def compare_snapshots(gs, rs, id_cap, where=""):
+    gg, gi = gs.snapshot(id_cap)
+    rg, ri = rs.snapshot(id_cap)
+    gg = gg.cpu().numpy(); gi = gi.cpu().numpy()
+    bad = np.argwhere(gg != rg)
+    assert bad.size == 0, f"{where}: GPU state differs at {bad[:5].tolist()}"
+    badi = np.argwhere(gi != ri)
+    assert badi.size == 0, (f"{where}: instance table differs at {badi[:5].tolist()}: "
+                            f"gpu {gi[tuple(badi[0][:2])].tolist()} ref {ri[tuple(badi[0][:2])].tolist()}")
+
+
+def compare_metrics(gs, rs, where=""):
+    gper, gtot = gs.metrics()
+    rper, rtot = rs.metrics()
+    gper = gper.cpu().numpy(); gtot = gtot.cpu().numpy()
+    if not np.array_equal(gper, rper):
+        bad = np.argwhere(gper != rper)
+        s, k = bad[0]
+        raise AssertionError(f"{where}: tally {di.TALLY_NAMES[k]} of scenario {s}: "
+                             f"gpu {gper[s, k]} ref {rper[s, k]} ({len(bad)} mismatches)")
+    assert np.array_equal(gtot, rtot)
+    return gtot
+
+
+def ratios(t):
+    """Final ratios (SURVEY s8(c) 'Final ratios'), host double from integers."""
+    act = max(int(t[T["gpu_slots_active"]]), 1)
+    return np.array([t[T["req_violated"]] / max(int(t[T["req_total"]]), 1),
+                     t[T["sm_unused_tokens"]] / act, t[T["mem_unused_mib_slots"]] / act])
+
+
+def run_pair(wl, chunks, id_cap=None, snap=True):
+    gs, rs = gpu_sim(wl), oracle.RefSim(wl)
+    id_cap = id_cap or 4 * wl.cfg["max_instances"]
+    done = 0
+    for n in chunks:
+        gs.scale_step(n)
+        rs.scale_step(n, threads=8)
+        done += n
+        if snap:
+            compare_snapshots(gs, rs, id_cap, f"{wl.name} slot {done}")
+    tot = compare_metrics(gs, rs, f"{wl.name} slot {done}")
+    np.testing.assert_allclose(ratios(tot), ratios(rs.metrics()[1]), rtol=1e-9)
+    return gs, rs, tot
+
+
+def test_c1_appendix_a():
+    wl = di.c1()
+    gs, rs, tot = run_pair(wl, [1, 4, 20, 15, 1, 1, 49, 1, 1, 7], id_cap=16)
+    assert tot[T["req_total"]] == 23610 and tot[T["req_violated"]] == 1250
+    assert tot[T["train_progress_tokens"]] == 114500000
+
+
+def test_c1_call_split_invariance():
+    wl = di.c1()
+    a = gpu_sim(wl); a.scale_step(100)
+    b = gpu_sim(wl)
+    for _ in range(100):
+        b.scale_step(1)
+    assert np.array_equal(a.metrics()[1].cpu().numpy(), b.metrics()[1].cpu().numpy())
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_c2_full_hour(seed):
+    wl = di.c2(seed=seed)
+    run_pair(wl, [1, 59, 540, 3000], id_cap=4096)
+
+
+def test_c4_sample_full_hour():
+    """C4 at full trace length on 48 scenarios spread over the 8^4 grid."""
+    full = di.c4(n_scenarios=4096)
+    wl = full.subset(np.arange(0, 4096, 87))
+    run_pair(wl, [3600], snap=False)
+
+
+@pytest.mark.parametrize("mode", ["threads64", "threads1024", "no_smem"])
+def test_launch_shape_invariance(mode, monkeypatch):
+    full = di.c4(n_scenarios=4096, T=600)
+    wl = full.subset(np.arange(5, 4096, 331))
+    if mode == "threads64":
+        monkeypatch.setenv("DILU_THREADS", "64")
+    elif mode == "threads1024":
+        monkeypatch.setenv("DILU_THREADS", "1024")
+    else:
+        monkeypatch.setenv("DILU_NO_SMEM", "1")
+    run_pair(wl, [600], id_cap=2048)
+
+
+def test_c3_window():
+    """C3 (1,024 GPUs, ~4,500 functions, state in HBM) for the first 30 minutes."""
+    wl = di.c3(T=86400)
+    run_pair(wl, [1, 299, 1500], id_cap=8192)
+
+
+def test_c5_shaped_reduced():
+    """C5-shaped (100 ms slots, diurnal mix) at reduced G for a full-trace parity."""
+    wl = di.scaled("C5r", 2048, 1300, 2500, 7500, 100, 3000, [50, 51], max_instances=32768)
+    run_pair(wl, [1, 9, 990, 2000], id_cap=20000)
+
+
+def test_place_batch_matches_oracle():
+    wl = di.c2(seed=3, T=300)
+    F = wl.cfg["max_funcs"]
+    rng = np.random.default_rng(0)
+    req_f = rng.integers(0, F, 150)
+    gs, rs = gpu_sim(wl), oracle.RefSim(wl)
+    g_gpu, g_iid = gs.place_batch(np.zeros(150, np.int32), req_f)
+    r_gpu, r_iid = rs.place_batch(np.zeros(150, np.int32), req_f)
+    assert np.array_equal(g_iid.cpu().numpy(), r_iid)
+    assert np.array_equal(g_gpu.cpu().numpy(), r_gpu)
+    compare_snapshots(gs, rs, 2048, "after place_batch")
+    gs.scale_step(300); rs.scale_step(300)
+    compare_snapshots(gs, rs, 4096, "after place_batch + 300 slots")
+    compare_metrics(gs, rs)
+
+
+def test_llm_split_heavy():
+    """Many LLM functions with big memory on few GPUs force worst-fit splits."""
+    wl = di.c4(n_scenarios=4096, T=900).subset(np.arange(0, 640, 61))
+    gs, rs, tot = run_pair(wl, [900], snap=False)
+    assert tot[T["llm_split_placements"]] > 0
+
+
+def test_capacity_error_matches():
+    wl = di.c2(seed=0, T=200, max_instances=100)
+    from paper_2503_05130_b200 import DiluError
+    gs = gpu_sim(wl)
+    gs.scale_step(200)
+    with pytest.raises(DiluError) as e:
+        gs.metrics()
+    assert e.value.code == 6
+    with pytest.raises(oracle.OracleError) as e2:
+        rs = oracle.RefSim(wl)
+        rs.scale_step(200)
+    assert e2.value.code == 6
+
+
+def test_degenerate_inputs():
+    """All rows unused; a single GPU; zero arrivals."""
+    wl = di.c1()
+    funcs = wl.funcs.copy()
+    funcs[:, :, 0] = -1
+    empty = di.Workload("empty", wl.cfg, wl.scen, funcs, wl.patterns, 100)
+    run_pair(empty, [100], id_cap=16)
+    one = di.c2(seed=4, T=120)
+    f1 = one.funcs.copy()
+    f1[:, :, di.FI["n_workers"]] = np.minimum(f1[:, :, di.FI["n_workers"]], 1)
+    one = di.Workload("G1", dict(one.cfg, gpus_per_scenario=1), one.scen, f1, one.patterns, 120)
+    run_pair(one, [120], id_cap=1024)
+    zero = di.c2(seed=5, T=120)
+    zero = di.Workload("zero", zero.cfg, zero.scen, zero.funcs, np.zeros_like(zero.patterns), 120)
+    run_pair(zero, [120], id_cap=1024)
