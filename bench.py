@@ -1,0 +1,315 @@
+#!/usr/bin/env python
+"""bench.py -- simulated GPU-slot decisions/s of the batched Dilu provisioning loop.
+
+Workload (default): C4 of BASELINE.json -- 4,096 independent 64-GPU scenarios (the
+rho x lambda x gamma x seed = 8^4 request/limit/oversubscription sweep), 200 functions
+each, one hour of 1 s slots.  One step = one full pass of the hot path over that batch:
+reset to slot 0 (inputs resident in HBM), 3,600 slots of boundary work (window push,
+departures, lazy scaling, arrivals, Alg.1 placement pass) and per-slot arrivals,
+dispatch, token allocation, gang minima and metric fold, then the device tally reduce
+and the one NCCL all-reduce of the int64 tally vector.  Decisions = sum over scenarios
+of G * slots (tally gpu_row_slots).
+
+Multi-GPU (torchrun): one rank per GPU.  Default --scaling weak: every rank runs its
+own 4,096-scenario replica of the sweep (distinct seeds and scenario ids), so per-GPU
+work is fixed; --scaling strong shards the 4,096 scenarios into contiguous blocks.
+Time = max over ranks of the summed CUDA-event step times; value = all ranks'
+decisions / that time.  L2 is flushed (256 MiB write) between timed steps.
+
+--impl reference times the CPU oracle (oracle/, plain C, all host cores) on a bounded
+sample of the same workload; only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "simulated GPU-slot decisions/sec"
+UNIT = "decisions/s"
+# Algorithmic integer operations per unit: counted from the oracle's
+# step definitions (oracle/dilu_ref.c), 64-bit ops counted once.
+OPS_PER_RESIDENT_SLOT = 65      # steps 7-9 for one warm (instance, stage): alloc, batches, fold, hash
+OPS_PER_FUNCTION_SLOT = 15      # step 6 for one registered inference function
+OPS_PER_FUNCTION_SECOND = 10    # steps 1 and 3 (window push, counts, decision)
+OPS_PER_GPU_SCORED = 15         # Alg.1 SelectOptGPU per candidate GPU per attempt
+OPS_PER_SCENARIO_SLOT = 6       # fold of active / memory tallies
+# INT32 issue peak: 148 SMs x (64 ALU-pipe + 64 FMA-pipe lanes)/clk x 1.965 GHz max clock
+# (B300_MICROARCH.md "fma vs alu split ... rt_SMSP=2"; B200_PROFILING.md SM count/clock)
+INT_PEAK_TOPS = 148 * 128 * 1.965e9 / 1e12
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dilu", choices=["dilu", "reference"])
+    ap.add_argument("--workload", default="C4", choices=["C4", "C2", "C3", "C5"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--slots", type=int, default=0, help="slots per step (0: workload default)")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample scenarios (0: auto)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+def build_workload(name: str, rank: int, world: int, scaling: str, slots: int):
+    import dilu_inputs as di
+    if name == "C4":
+        if scaling == "weak":
+            wl = di.c4(n_scenarios=4096, T=slots or 3600, replica=rank)
+            desc = "C4 replica %d: 4096 x 64-GPU scenarios (rho x lambda x gamma x seed sweep)" % rank
+        else:
+            lo, hi = 4096 * rank // world, 4096 * (rank + 1) // world
+            wl = di.c4(n_scenarios=hi - lo, first=lo, T=slots or 3600)
+            desc = "C4 scenarios [%d, %d) of 4096 x 64-GPU sweep" % (lo, hi)
+        return wl, desc, wl.n_slots
+    if name == "C2":
+        wl = di.c2(seed=rank, T=slots or 3600)
+        return wl, "C2: one 64-GPU cluster, 200 functions, bursty", wl.n_slots
+    if name == "C3":
+        wl = di.c3(seed=rank, T=86400)
+        return wl, "C3: one 1,024-GPU cluster, ~4,500 functions, diurnal", slots or 3600
+    if name == "C5":
+        T = slots or 36000
+        n = 8 if scaling == "weak" else max(1, 8 // world)
+        first = 50 + (8 * rank if scaling == "weak" else n * rank)
+        wl = di.c5(n_scenarios=n, T=T, first_seed=first)
+        return wl, "C5: %d x 16,384-GPU clusters, 100 ms slots, timed window" % n, T
+    raise ValueError(name)
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        import statistics
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_baseline(wl, n_slots: int, sample: int, threads: int):
+    """The oracle, as it stands, on a bounded sample of the same workload (rank 0, N=1)."""
+    import numpy as np
+    import oracle
+    S = wl.S
+    sample = max(1, min(S, sample))
+    idx = np.linspace(0, S - 1, sample).round().astype(int)
+    sub = wl.subset(idx) if S > 1 else wl
+    s = oracle.RefSim(sub)
+    t0 = time.perf_counter()
+    s.scale_step(n_slots, threads)
+    dt = time.perf_counter() - t0
+    _, tot = s.metrics()
+    s.close()
+    D = int(tot[15])
+    return D / dt, dt, sample, D
+
+
+def run_reference(args):
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    if rank != 0:
+        return
+    wl, desc, n_slots = build_workload(args.workload, 0, 1, args.scaling, args.slots)
+    cores = len(os.sched_getaffinity(0))
+    sample = args.cpu_sample or max(cores, min(wl.S, 2 * cores))
+    vals = []
+    for k in range(args.warmup + args.steps):
+        v, dt, n, D = cpu_baseline(wl, n_slots, sample, cores)
+        if k >= args.warmup:
+            vals.append((v, dt, D))
+    tot_D = sum(x[2] for x in vals)
+    tot_t = sum(x[1] for x in vals)
+    value = tot_D / tot_t
+    smp = f"{sample} of {wl.S} scenarios x {n_slots} slots per step ({desc})"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * tot_t / len(vals), "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic", "config": {"workload": desc, "slots": n_slots},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": smp},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_dilu(args):
+    import numpy as np
+    import torch
+    from paper_2503_05130_b200 import DiluSim, dist as ddist
+    rank, world = ddist.init("nccl")
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    wl, desc, n_slots = build_workload(args.workload, rank, world, args.scaling, args.slots)
+    sim = DiluSim.from_workload(wl, device=dev)
+    stream = sim.stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    tally = torch.zeros(17, dtype=torch.int64, device=dev)
+
+    def step(ev=None):
+        sim.reset()
+        if ev:
+            ev[0].record(stream)
+        sim.scale_step(n_slots)
+        if ev:
+            ev[1].record(stream)
+        _, tot = sim.metrics(per_scenario=False)
+        tally.copy_(tot)
+        ddist.allreduce_tallies(tally)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    step_ms, kern_ms = [], []
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)                       # L2 flush between timed steps
+            torch.cuda.synchronize()
+            ddist.barrier()
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record(stream)
+            step(ev=(e[2], e[3]))
+            e[1].record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(e[0].elapsed_time(e[1]))
+            kern_ms.append(e[2].elapsed_time(e[3]))
+        ddist.barrier()
+    local_ms = sum(step_ms)
+    max_ms = ddist.allreduce_max(local_ms)
+    D_local = int(sim.metrics(per_scenario=False)[1][15].item())
+    D_all = int(tally[15].item())                        # all ranks (after the all-reduce)
+    value = D_all * args.steps / (max_ms / 1000.0)
+    stats = sim.kernel_stats()
+
+    # roofline of the dominant kernel (k_run = the scale_step launch), algorithmic ops
+    sps = 1000 // wl.cfg["slot_ms"]
+    ops = (OPS_PER_RESIDENT_SLOT * stats["resident_slots"]
+           + OPS_PER_FUNCTION_SLOT * stats["function_slots"]
+           + OPS_PER_FUNCTION_SECOND * stats["function_slots"] // sps
+           + OPS_PER_GPU_SCORED * wl.G * stats["attempts"]
+           + OPS_PER_SCENARIO_SLOT * stats["slots"])
+    k_s = sum(kern_ms) / len(kern_ms) / 1000.0
+    achieved = ops / k_s / 1e12
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = prof.get(args.workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    # end to end through the public API: pinned host inputs -> create (H2D) -> slots ->
+    # tallies D2H into pinned host memory, every step
+    e2e_val, h2d, d2h = None, 0, 0
+    if args.e2e_steps > 0:
+        pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(wl, k))).pin_memory()
+               for k in ("scen", "funcs", "patterns")}
+        h2d = sum(t.numel() * t.element_size() for t in pin.values())
+        d2h = 17 * 8
+        times = []
+        for k in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            ddist.barrier()
+            t0 = time.perf_counter()
+            s2 = DiluSim(wl.cfg_array(), pin["scen"].numpy(), pin["funcs"].numpy(),
+                         pin["patterns"].numpy(), device=dev)
+            s2.scale_step(n_slots)
+            _, tot = s2.metrics(per_scenario=False, host=True)
+            times.append(time.perf_counter() - t0)
+            s2.close()
+            del s2
+        e2e_s = ddist.allreduce_max(sum(times))
+        e2e_val = D_local * world * len(times) / e2e_s
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = len(os.sched_getaffinity(0))
+        sample = args.cpu_sample or (max(cores, 96) if args.workload == "C4" else 1)
+        v, dt, n, D = cpu_baseline(wl, n_slots if args.workload != "C5" else min(n_slots, 600),
+                                   sample, cores)
+        cpu = {"value": v, "unit": UNIT, "cores": min(cores, n), "kind": "oracle",
+               "sample": f"{n} of {wl.S} scenarios x {n_slots if args.workload != 'C5' else min(n_slots, 600)} "
+                         f"slots, one pthread per scenario, {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": desc, "scenarios_per_gpu": wl.S, "gpus_per_scenario": wl.G,
+                       "slots": n_slots, "slot_ms": wl.cfg["slot_ms"], "decisions_per_step": D_all,
+                       "l2": "flushed between timed steps (256 MiB write)",
+                       "parallelism": f"scenario shards x{world}"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": INT_PEAK_TOPS,
+                         "unit": "Tops/s", "frac": achieved / INT_PEAK_TOPS, "traffic": traffic,
+                         "kernel": "k_run (one launch per step)", "kernel_ms": 1000 * k_s,
+                         "ops_per_launch": ops, "peak_source": "derived (DESIGN.md s7)"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": 3 * args.steps,
+            "clocks": clk.summary(),
+            "kernel_stats_per_step": stats,
+        }
+        print(json.dumps(line), flush=True)
+    ddist.barrier()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_dilu(args)
+
+
+if __name__ == "__main__":
+    main()

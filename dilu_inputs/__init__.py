@@ -300,13 +300,15 @@ C4_GAMMA = [1.0, 1.125, 1.25, 1.375, 1.5, 1.75, 2.0, 2.5]
 
 
 def c4(n_scenarios: int = 4096, T: int = 3600, max_instances: int = 512,
-       first: int = 0) -> Workload:
+       first: int = 0, replica: int = 0) -> Workload:
     """4,096 C2-shaped scenarios: sweep rho x lambda x gamma x seed = 8^4.
     Scenario id = seed + 8*(gamma_i + 8*(lambda_i + 8*rho_i)).  ``first``/``n_scenarios``
-    select a contiguous id range of the full grid."""
+    select a contiguous id range of the full grid.  ``replica`` r > 0 draws the 8 fleet
+    seeds from 8r..8r+7 and offsets ids by 4096r (weak-scaling copies of the sweep, one
+    per rank)."""
     pats = make_patterns(T, 1000, 4000, diurnal=False)
     bases = []
-    for seed in range(8):
+    for seed in range(8 * replica, 8 * replica + 8):
         bases.append(_fleet(_rng(seed, "fleet"), 40, 40, 120, 1000, T, pats, BURSTY_FAMILY,
                             inf_arrive_frac0=1.0, inf_life_s=(0, 0),
                             train_arrive_max_s=T, train_len_s=(600, 2400),
@@ -330,7 +332,8 @@ def c4(n_scenarios: int = 4096, T: int = 3600, max_instances: int = 512,
     funcs[:, :, FI["req_pm"]] = np.where(used, req2, funcs[:, :, FI["req_pm"]])
     funcs[:, :, FI["lim_pm"]] = np.where(used, lim2, funcs[:, :, FI["lim_pm"]])
     gam = (np.array(C4_GAMMA)[gam_i] * 1000 + 0.5).astype(np.int32)
-    scen = np.stack([ids, np.full_like(ids, 1000), gam, np.zeros_like(ids)], axis=1).astype(np.int32)
+    scen = np.stack([ids + 4096 * replica, np.full_like(ids, 1000), gam, np.zeros_like(ids)],
+                    axis=1).astype(np.int32)
     cfg = default_config(n_scenarios=int(n_scenarios), gpus_per_scenario=64,
                          max_funcs=funcs.shape[1], max_instances=max_instances, n_patterns=64,
                          pattern_len=T)

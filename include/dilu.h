@@ -158,7 +158,8 @@ dilu_status dilu_snapshot(dilu_sim* s, int32_t id_cap, int32_t* d_gpu, int32_t* 
 /* Diagnostics (tracing; off the timed path): per-scenario int64 [n_scenarios][8] (may
  * be NULL) and their sum [8] (may be NULL) of kernel counters accumulated since the
  * last create/reset: full placement attempts, retry-skip checks, row repacks, boundary
- * events, queue scans, slots simulated, 2 reserved.  Host or device pointers.
+ * events, queue scans, slots simulated, warm resident-slots allocated, inference
+ * function-slots dispatched.  Host or device pointers.
  * Synchronises the stream. */
 dilu_status dilu_kernel_stats(dilu_sim* s, int64_t* per_scenario, int64_t* sum);
 

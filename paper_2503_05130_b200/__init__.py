@@ -160,7 +160,7 @@ class DiluSim:
         return gpu, inst[:, :id_cap]
 
     STAT_NAMES = ["attempts", "retry_checks", "row_repacks", "boundary_events", "queue_scans",
-                  "slots", "reserved0", "reserved1"]
+                  "slots", "resident_slots", "function_slots"]
 
     def kernel_stats(self):
         """Diagnostics: dict of summed kernel counters (dilu_kernel_stats)."""

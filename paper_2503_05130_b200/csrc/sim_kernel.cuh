@@ -44,10 +44,11 @@ struct Acc0 {  // thread-0 tallies, kept in shared memory (not in every thread's
   long long act, memu, rows, pok, pfail, cold, sout, sin, split, maxa;
   long long st[NSTAT];   // statistics: attempts, hope checks, relayouts, events, scanned, slots
 };
-enum { S_ATTEMPT = 0, S_HOPE, S_LAYOUT, S_EVENT, S_SCAN, S_SLOT };
+enum { S_ATTEMPT = 0, S_HOPE, S_LAYOUT, S_EVENT, S_SCAN, S_SLOT, S_RES, S_FUN };
 struct Acc {   // per-thread tallies
   long long rtot, rsrv, rvio, iexe, tprg, etot;
   unsigned long long hash;
+  int32_t nres, nfun;   // statistics: warm resident-slots (P1), inference function-slots (P0)
   Acc0* z;     // shared, written by thread 0 only
 };
 
@@ -577,6 +578,7 @@ __device__ void phase0(Scn& c, int32_t t, Acc& acc) {
     pidx[f] = idx + 1 == Tp ? 0 : idx + 1;
     const long long x = __ldg(gpat + (size_t)fpat[f] * Tp + idx);
     const int32_t A = (int32_t)((x * fscale[f]) >> 10);
+    acc.nfun += 1;
     facc[f] += A;
     acc.rtot += A;
     int32_t nw = 0;
@@ -673,6 +675,7 @@ __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
       const int32_t room = T - sreq - (incl - want);
       const int32_t sp = want < room ? want : (room > 0 ? room : 0);
       const int32_t a = req + sp;
+      acc.nres += 1;
       acc.hash += sm64(sm64(ht ^ (uint32_t)iid[s]) ^ ((uint64_t((uint32_t)g) << 32) | (uint32_t)a));
       if (kind == K_TRAIN) {
         atomicMin(&gang[f], d < a ? d : a);              // x = min(d, a)
@@ -963,18 +966,18 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
   // ---- block-reduce the tallies once per call
   {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    long long vals[7] = {acc.rtot, acc.rsrv, acc.rvio, acc.iexe, acc.tprg, acc.etot,
-                         (long long)acc.hash};
+    long long vals[9] = {acc.rtot, acc.rsrv, acc.rvio, acc.iexe, acc.tprg, acc.etot,
+                         (long long)acc.hash, acc.nres, acc.nfun};
 #pragma unroll
-    for (int q = 0; q < 7; ++q) {
+    for (int q = 0; q < 9; ++q) {
       long long x = vals[q];
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
       if (lane == 0) red.acc[q][wid] = x;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      long long s7[7] = {0, 0, 0, 0, 0, 0, 0};
-      for (int q = 0; q < 7; ++q)
+      long long s7[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int q = 0; q < 9; ++q)
         for (int k = 0; k < nw; ++k)
           s7[q] = (long long)((unsigned long long)s7[q] + (unsigned long long)red.acc[q][k]);
       long long* T = reinterpret_cast<long long*>(P.tally) + (size_t)sc * NT;
@@ -996,6 +999,8 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
       T[T_ROWS] += acc.z->rows;
       if (acc.z->maxa > T[T_MAXA]) T[T_MAXA] = acc.z->maxa;
       long long* ST = reinterpret_cast<long long*>(P.stats) + (size_t)sc * NSTAT;
+      acc.z->st[S_RES] += s7[7];
+      acc.z->st[S_FUN] += s7[8];
       for (int k = 0; k < NSTAT; ++k) ST[k] += acc.z->st[k];
     }
   }
