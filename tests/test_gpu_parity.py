@@ -94,17 +94,31 @@ def test_c4_sample_full_hour():
     run_pair(wl, [3600], snap=False)
 
 
-@pytest.mark.parametrize("mode", ["threads64", "threads1024", "no_smem"])
+@pytest.mark.parametrize("mode", ["cta_threads64", "cta_threads1024", "cta_no_smem", "lanes_p4",
+                                  "lanes_p16", "lanes_p8"])
 def test_launch_shape_invariance(mode, monkeypatch):
+    """Both engines and several launch shapes give bit-identical results (45 scenarios:
+    a partial 32-scenario group for the lanes engine)."""
     full = di.c4(n_scenarios=4096, T=600)
-    wl = full.subset(np.arange(5, 4096, 331))
-    if mode == "threads64":
+    wl = full.subset(np.arange(5, 4096, 91))
+    engine, _, shape = mode.partition("_")
+    monkeypatch.setenv("DILU_ENGINE", engine)
+    if shape == "threads64":
         monkeypatch.setenv("DILU_THREADS", "64")
-    elif mode == "threads1024":
+    elif shape == "threads1024":
         monkeypatch.setenv("DILU_THREADS", "1024")
-    else:
+    elif shape == "no_smem":
         monkeypatch.setenv("DILU_NO_SMEM", "1")
-    run_pair(wl, [600], id_cap=2048)
+    elif shape.startswith("p"):
+        monkeypatch.setenv("DILU_PARTS", shape[1:])
+    run_pair(wl, [1, 599], id_cap=2048)
+
+
+@pytest.mark.parametrize("engine", ["cta", "lanes"])
+def test_engines_on_c1_c2(engine, monkeypatch):
+    monkeypatch.setenv("DILU_ENGINE", engine)
+    run_pair(di.c1(), [1, 39, 1, 59], id_cap=16)
+    run_pair(di.c2(seed=5, T=900), [1, 299, 600], id_cap=4096)
 
 
 def test_c3_window():
