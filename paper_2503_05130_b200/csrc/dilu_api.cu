@@ -21,7 +21,8 @@ using namespace dilu;
 
 struct dilu_sim {
   dilu_config cfg;
-  int engine;          // 0: CTA per scenario (large scenarios), 1: lanes (32 scenarios per CTA)
+  int engine;          // 0: CTA per scenario, 1: lanes (32 scenarios per CTA), 2: cluster per scenario
+  int K;               // cluster engine: CTAs per scenario
   int parts;           // lanes engine: warps per scenario group
   Layout L;
   Params P;
@@ -46,7 +47,7 @@ constexpr size_t ALIGN = 256;
 inline size_t up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
 
 struct Carve {
-  size_t funcs, pat, scen, state, ring, tally, stats, sum, total;
+  size_t funcs, pat, scen, state, ring, tally, stats, gscr, sum, total;
 };
 
 bool check_cfg(const dilu_config* c, char* msg, size_t n) {
@@ -120,9 +121,10 @@ bool check_inputs(const dilu_config* c, const dilu_scenario* scen, const dilu_fu
 // Default: the CTA engine for every config (measured fastest); the lanes
 // engine (32 scenarios per CTA) is available for small scenarios and is parity-tested.
 int choose_engine(const dilu_config* c) {
-  int e = 0;
+  int e = c->gpus_per_scenario > 256 ? 2 : 0;   // large scenarios: a cluster each
   if (const char* v = getenv("DILU_ENGINE")) {
     if (!strcmp(v, "cta")) e = 0;
+    if (!strcmp(v, "cluster")) e = 2;
     if (!strcmp(v, "lanes") && c->gpus_per_scenario <= 256 && c->max_funcs <= 4096 &&
         c->max_instances <= 8192)
       e = 1;
@@ -158,6 +160,7 @@ Carve carve(const dilu_config* c, const Layout& L) {
   }
   k.tally = o; o = up(o + S * NT * 8);
   k.stats = o; o = up(o + S * NSTAT * 8);
+  k.gscr = o; o = up(o + S * GSCR * 8);
   k.sum = o; o = up(o + (NT + 2) * 8);
   k.total = o;
   return k;
@@ -198,6 +201,24 @@ dilu_status launch_run(dilu_sim* s, int32_t n_slots, int32_t n_req, const int32_
   dilu_status rc = cuda_check(s, cudaMemsetAsync(s->d_next, 0, sizeof(int32_t), s->stream), "counter reset");
   if (rc) return rc;
   const dim3 grid(s->grid), block(s->threads);
+  if (s->engine == 2) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(s->cfg.n_scenarios * s->K);
+    lc.blockDim = dim3(s->threads);
+    lc.dynamicSmemBytes = 0;
+    lc.stream = s->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = s->K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    rc = cuda_check(s, cudaLaunchKernelEx(&lc, k_run_cluster, s->P, s->t, n_slots, n_req, rs, rf, og, oi),
+                    "k_run_cluster launch");
+    if (rc) return rc;
+    return cuda_check(s, cudaGetLastError(), "k_run_cluster");
+  }
   if (s->engine == 1) {
     switch (s->parts) {
       case 4: lanes::k_lanes<4><<<grid, block, 0, s->stream>>>(s->LP, s->d_next, s->t, n_slots, n_req, rs, rf, og, oi); break;
@@ -286,6 +307,7 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   P.ring = reinterpret_cast<int32_t*>(s->ws + k.ring);
   P.tally = reinterpret_cast<int64_t*>(s->ws + k.tally);
   P.stats = reinterpret_cast<int64_t*>(s->ws + k.stats);
+  P.gscratch = reinterpret_cast<unsigned long long*>(s->ws + k.gscr);
   P.L = s->L;
   P.S = cfg->n_scenarios; P.G = cfg->gpus_per_scenario; P.F = cfg->max_funcs;
   P.I = cfg->max_instances; P.W = cfg->window_s; P.M = cfg->mem_mib; P.Q = cfg->q_pm;
@@ -311,6 +333,35 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
     s->threads = 32 * s->parts;
     s->use_smem = false;
     s->grid = Q.ngroups;       // one persistent CTA per group: every group resident
+    return dilu_sim_reset(s);
+  }
+  if (s->engine == 2) {
+    s->threads = 1024;
+    s->use_smem = false;
+    if ((rc = cuda_check(s, cudaFuncSetAttribute(k_run_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                         "cluster attribute")))
+      return rc;
+    int n_sm = 0;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    int want = n_sm / (cfg->n_scenarios > 0 ? cfg->n_scenarios : 1);
+    if (const char* e = getenv("DILU_CLUSTER")) want = atoi(e);
+    int K = want >= 16 ? 16 : (want >= 8 ? 8 : (want >= 4 ? 4 : (want >= 2 ? 2 : 1)));
+    for (; K >= 1; K /= 2) {           // largest cluster the device can schedule
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(K);
+      lc.blockDim = dim3(s->threads);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = K; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, k_run_cluster, &lc) == cudaSuccess && nclusters > 0) break;
+      cudaGetLastError();
+    }
+    if (K < 1) return fail(s, DILU_E_CUDA, "no schedulable cluster size");
+    s->K = K;
+    s->grid = cfg->n_scenarios * K;
     return dilu_sim_reset(s);
   }
   // CTA engine launch shape: one CTA per scenario; hot state in shared memory when it fits
@@ -406,7 +457,7 @@ dilu_status dilu_scale_step(dilu_sim* s, int32_t n_slots) {
 dilu_status dilu_metrics(dilu_sim* s, int64_t* per_scenario, int64_t* sum) {
   if (!s) return DILU_E_USAGE;
   if (s->status == DILU_E_CUDA) return DILU_E_STATE;
-  k_sum_err<<<1, 32, 0, s->stream>>>(s->P, s->d_sum, s->engine == 0);
+  k_sum_err<<<1, 32, 0, s->stream>>>(s->P, s->d_sum, s->engine != 1);
   if (s->engine == 1) lanes::k_lanes_errs<<<1, 32, 0, s->stream>>>(s->LP, s->d_sum + NT);
   dilu_status rc = cuda_check(s, cudaGetLastError(), "k_sum launch");
   if (rc) return rc;

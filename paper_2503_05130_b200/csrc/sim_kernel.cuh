@@ -34,11 +34,14 @@ struct Params {
   int32_t* ring;             // [S][F][W]
   int64_t* tally;            // [S][NT]
   int64_t* stats;            // [S][NSTAT] kernel statistics
+  unsigned long long* gscratch;  // [S][GSCR] cluster-collective scratch
   Layout L;
   int32_t S, G, F, I, W, M, Q, aw, bw, slot_ms, SPS, phi_out, phi_in, min_inst, max_stages,
       flags, Tp;
   int64_t T_slot;
 };
+
+constexpr int GSCR = 96;     // u64 words of per-scenario cluster scratch
 
 struct Acc0 {  // thread-0 tallies, kept in shared memory (not in every thread's registers)
   long long act, memu, rows, pok, pfail, cold, sout, sin, split, maxa;
@@ -122,11 +125,41 @@ __device__ __forceinline__ int32_t block_scan_i32(int32_t v, Red& r, int& phase,
   return before + x - v;
 }
 
+// ------------------------------------------------------------------ groups
+//
+// The threads that run one scenario: one CTA (K = 1), or a thread-block cluster of K
+// CTAs (large scenarios, state in HBM/L2).  Cluster-wide collectives are the CTA-level
+// ones followed by one hardware cluster barrier (release/acquire, which also makes the
+// other CTAs' global writes visible) over a small per-scenario global scratch.
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+
+struct Grp {
+  int K, crank, cph;
+  unsigned long long* gu;    // [2][16] cluster scratch (u64)
+  int32_t* gi;               // [2][16] cluster scratch (i32)
+  __device__ int rank() const { return crank * blockDim.x + threadIdx.x; }
+  __device__ int size() const { return K * blockDim.x; }
+  __device__ int wrank() const { return (crank * blockDim.x + threadIdx.x) >> 5; }
+  __device__ int nwarps() const { return (K * blockDim.x) >> 5; }
+  __device__ bool leader() const { return crank == 0 && threadIdx.x == 0; }
+  __device__ bool lead_warp() const { return crank == 0 && threadIdx.x < 32; }
+  __device__ void sync() const {
+    if (K == 1) __syncthreads(); else cluster_sync_all();
+  }
+};
+
 // ------------------------------------------------------------------ scenario
 
 struct Scn {
   View& v;                   // lives in shared memory (one per CTA), not in registers
   const Params* P;
+  Grp g;
+  int32_t* members;          // gang member slots of the request being placed (group-visible)
+  int32_t* flag;             // group-visible broadcast word
   const int32_t* frow;       // this scenario's input function rows [F][16]
   int32_t scn_id, om, ga;
 };
@@ -134,6 +167,49 @@ struct Scn {
 __device__ __forceinline__ int st_of(int32_t meta) { return meta & 3; }
 __device__ __forceinline__ int nst_of(int32_t meta) { return (meta >> 4) & 7; }
 __device__ __forceinline__ bool is_inf(int32_t k) { return k == K_INF || k == K_LLM; }
+
+// ---- group collectives (K = 1: CTA-level; K > 1: CTA-level then one cluster barrier) --
+
+__device__ unsigned long long g_min_u64(Scn& c, unsigned long long v, Red& red, int& ph) {
+  v = block_min_u64(v, red, ph);
+  if (c.g.K == 1) return v;
+  unsigned long long* buf = c.g.gu + (c.g.cph & 1) * 16;
+  if (threadIdx.x == 0) buf[c.g.crank] = v;
+  c.g.cph ^= 1;
+  cluster_sync_all();
+  unsigned long long m = ~0ull;
+  for (int k = 0; k < c.g.K; ++k) { const unsigned long long x = __ldcg(buf + k); m = x < m ? x : m; }
+  return m;
+}
+__device__ int32_t g_sum_i32(Scn& c, int32_t cta_value) {   // cta_value uniform within the CTA
+  if (c.g.K == 1) return cta_value;
+  int32_t* buf = c.g.gi + (c.g.cph & 1) * 16;
+  if (threadIdx.x == 0) buf[c.g.crank] = cta_value;
+  c.g.cph ^= 1;
+  cluster_sync_all();
+  int32_t r = 0;
+  for (int k = 0; k < c.g.K; ++k) r += __ldcg(buf + k);
+  return r;
+}
+__device__ bool g_any(Scn& c, bool p) { return g_sum_i32(c, __syncthreads_or(p)) != 0; }
+__device__ int32_t g_count(Scn& c, int p) { return g_sum_i32(c, __syncthreads_count(p)); }
+__device__ int32_t g_scan(Scn& c, int32_t v, Red& red, int& ph, int32_t* total) {
+  int32_t ctot;
+  const int32_t pre = block_scan_i32(v, red, ph, &ctot);
+  if (c.g.K == 1) { *total = ctot; return pre; }
+  int32_t* buf = c.g.gi + (c.g.cph & 1) * 16;
+  if (threadIdx.x == 0) buf[c.g.crank] = ctot;
+  c.g.cph ^= 1;
+  cluster_sync_all();
+  int32_t before = 0, tot = 0;
+  for (int k = 0; k < c.g.K; ++k) {
+    const int32_t x = __ldcg(buf + k);
+    if (k < c.g.crank) before += x;
+    tot += x;
+  }
+  *total = tot;
+  return before + pre;
+}
 
 // ---- serial helpers (thread 0 only) ------------------------------------------------
 
@@ -296,7 +372,7 @@ __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
   const long long aM = (long long)P.aw * P.M, bQ = (long long)P.bw * P.Q;
   const unsigned long long MASK40 = (1ull << 40) - 1;
   unsigned long long best = ~0ull;
-  for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
+  for (int32_t g = c.g.rank(); g < P.G; g += c.g.size()) {
     if (v.gExcl[g]) continue;
     const int32_t n = v.gN[g];
     unsigned long long key;
@@ -314,11 +390,11 @@ __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
     }
     best = key < best ? key : best;
   }
-  best = block_min_u64(best, red, ph);
+  best = g_min_u64(c, best, red, ph);
   const int tier = best == ~0ull ? 3 : (int)(best >> 62);
   if (tier <= 1) {
-    if (threadIdx.x == 0) commit(c, s, (int32_t)(best & 0x3FFFFF), mem);
-    __syncthreads();
+    if (c.g.leader()) commit(c, s, (int32_t)(best & 0x3FFFFF), mem);
+    c.g.sync();
     return true;
   }
   if (v.fKind[f] == K_LLM && (P.flags & 1)) {
@@ -330,7 +406,7 @@ __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
     bool okk = false;
     for (int r = 0; r < P.max_stages; ++r) {
       unsigned long long kk = ~0ull;
-      for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
+      for (int32_t g = c.g.rank(); g < P.G; g += c.g.size()) {
         const int32_t n = v.gN[g];
         if (n == 0 || v.gExcl[g] || n >= RES) continue;
         bool dup = false;
@@ -343,7 +419,7 @@ __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
             ((unsigned long long)(0xFFFFFFFFu - (uint32_t)fr) << 32) | (uint32_t)g;
         kk = key < kk ? key : kk;
       }
-      kk = block_min_u64(kk, red, ph);
+      kk = g_min_u64(c, kk, red, ph);
       if (kk == ~0ull) break;
       picked[r] = (int32_t)(kk & 0xFFFFFFFFu);
       pfree[r] = (int32_t)(0xFFFFFFFFu - (uint32_t)(kk >> 32));
@@ -352,7 +428,7 @@ __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
       if (sum >= mem) { okk = true; break; }
     }
     if (okk) {
-      if (threadIdx.x == 0) {
+      if (c.g.leader()) {
         int32_t left = mem;
         for (int j = 0; j < k; ++j) {
           const int32_t sh = pfree[j] < left ? pfree[j] : left;
@@ -360,13 +436,13 @@ __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
           left -= sh;
         }
       }
-      __syncthreads();
+      c.g.sync();
       return true;
     }
   }
   if (tier == 2) {
-    if (threadIdx.x == 0) commit(c, s, (int32_t)(best & 0x3FFFFF), mem);
-    __syncthreads();
+    if (c.g.leader()) commit(c, s, (int32_t)(best & 0x3FFFFF), mem);
+    c.g.sync();
     return true;
   }
   return false;
@@ -456,39 +532,39 @@ __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
   bool removed = false;
   int32_t q = 0;
   for (;;) {
-    if (threadIdx.x < 32) {
+    if (c.g.lead_warp()) {
       const int32_t e = next_attempt(c, q, qn, acc);
-      if (threadIdx.x == 0) red.flag = e;
+      if (threadIdx.x == 0) *c.flag = e;
     }
-    __syncthreads();
-    q = red.flag;
+    c.g.sync();
+    q = c.g.K == 1 ? *c.flag : __ldcg(c.flag);
     if (q >= qn) break;
     const int32_t n = v.qN[q];
     const int32_t f = v.qFunc[q], first = v.qFirst[q];
-    if (threadIdx.x == 0) {          // gang members, ascending id
+    if (c.g.leader()) {              // gang members, ascending id
       int j = 0;
       for (int32_t s = v.fLh[f]; s >= 0 && j < n; s = v.iNext[s]) {
         const int32_t id = v.iId[s];
-        if (id >= first && id < first + n) red.members[j++] = s;
+        if (id >= first && id < first + n) c.members[j++] = s;
       }
+      acc.z->st[S_ATTEMPT] += 1;
     }
-    __syncthreads();
+    c.g.sync();
     int placed = 0;
-    if (threadIdx.x == 0) acc.z->st[S_ATTEMPT] += 1;
     for (int j = 0; j < n; ++j) {
-      if (!place_one(c, red, ph, red.members[j])) break;
+      if (!place_one(c, red, ph, c.g.K == 1 ? c.members[j] : __ldcg(c.members + j))) break;
       ++placed;
     }
-    if (threadIdx.x == 0) {
+    if (c.g.leader()) {
       for (int j = 0; j < placed; ++j) {   // clear I* marks
-        const int32_t s = red.members[j];
+        const int32_t s = c.members[j];
         const int ns = nst_of(v.iMeta[s]);
         for (int k = 0; k < ns; ++k) v.gExcl[v.iG[s * MAXST + k]] = 0;
       }
       if (placed == n) {
         const int32_t cold = v.fCold[f];
         for (int j = 0; j < n; ++j) {
-          const int32_t s = red.members[j];
+          const int32_t s = c.members[j];
           v.iMeta[s] = (v.iMeta[s] & ~3) | ST_PLACED;
           v.iReady[s] = t + cold;
           acc.z->pok += 1;
@@ -498,15 +574,15 @@ __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
         v.qN[q] = 0;
         removed = true;
       } else {
-        for (int j = 0; j < placed; ++j) release(c, red.members[j]);  // rollback
+        for (int j = 0; j < placed; ++j) release(c, c.members[j]);  // rollback
         acc.z->pfail += 1;
         v.qFail[q] = v.h[H_EPOCH];
       }
     }
-    __syncthreads();
+    c.g.sync();
     ++q;
   }
-  if (threadIdx.x == 0 && removed) compact_queue(v);
+  if (c.g.leader() && removed) compact_queue(v);
 }
 
 // ---- B5: pack GPU rows into 32-lane warp chunks by width class (1..32 lanes) ----------
@@ -518,14 +594,14 @@ __device__ __forceinline__ int width_class(int32_t n) {
 __device__ void rebuild_layout(Scn& c) {
   View& v = c.v;
   const Params& P = *c.P;
-  if (threadIdx.x < 6) { v.h[H_CCNT + threadIdx.x] = 0; v.h[H_CCNT2 + threadIdx.x] = 0; }
-  __syncthreads();
-  for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
+  if (c.g.crank == 0 && threadIdx.x < 6) { v.h[H_CCNT + threadIdx.x] = 0; v.h[H_CCNT2 + threadIdx.x] = 0; }
+  c.g.sync();
+  for (int32_t g = c.g.rank(); g < P.G; g += c.g.size()) {
     const int32_t n = v.gN[g];
     if (n > 0) atomicAdd(&v.h[H_CCNT + width_class(n)], 1);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  c.g.sync();
+  if (c.g.leader()) {
     int32_t cb = 0, gb = 0;
     for (int k = 0; k < 6; ++k) {
       v.h[H_CBASE + k] = cb;
@@ -537,8 +613,8 @@ __device__ void rebuild_layout(Scn& c) {
     v.h[H_CBASE + 6] = cb;
     v.h[H_DIRTY] = 0;
   }
-  __syncthreads();
-  for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
+  c.g.sync();
+  for (int32_t g = c.g.rank(); g < P.G; g += c.g.size()) {
     const int32_t n = v.gN[g];
     if (n > 0) {
       const int k = width_class(n);
@@ -546,7 +622,7 @@ __device__ void rebuild_layout(Scn& c) {
       v.gGrow[v.h[H_GBASE + k] + idx] = g;   // order inside a class is irrelevant
     }
   }
-  __syncthreads();
+  c.g.sync();
 }
 
 // ---- per-slot phases ------------------------------------------------------------------
@@ -571,7 +647,7 @@ __device__ void phase0(Scn& c, int32_t t, Acc& acc) {
   int32_t* __restrict__ r = v.iR + (t & 1) * P.I;
   const int32_t* __restrict__ gpat = P.pat;
   const int32_t Tp = P.Tp, ninf = v.h[H_NINF];
-  for (int32_t k = threadIdx.x; k < ninf; k += blockDim.x) {
+  for (int32_t k = c.g.rank(); k < ninf; k += c.g.size()) {
     const int32_t f = infl[k];
     if (!reg[f]) continue;
     const int32_t idx = pidx[f];
@@ -600,7 +676,7 @@ __device__ void phase0(Scn& c, int32_t t, Acc& acc) {
 __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
   View& v = c.v;
   const Params& P = *c.P;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
   const int par = t & 1;
   const int32_t* __restrict__ r = v.iR + par * P.I;
   int32_t* bmin = v.iBmin + par * P.I;
@@ -713,7 +789,7 @@ __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
   const int32_t* __restrict__ nxt = v.iNext;
   const int32_t* __restrict__ meta = v.iMeta;
   const int32_t ndef = v.h[H_NDEF];
-  for (int32_t k = threadIdx.x; k < ndef; k += blockDim.x) {
+  for (int32_t k = c.g.rank(); k < ndef; k += c.g.size()) {
     const int32_t f = defl[k];
     if (!reg[f]) continue;
     if (v.fKind[f] == K_TRAIN) {
@@ -779,8 +855,8 @@ __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
   int32_t* __restrict__ fflag = v.fFlag;
   int32_t* __restrict__ ringb = v.ring;
   const int32_t W = P.W;
-  const int32_t per = (P.F + blockDim.x - 1) / blockDim.x;
-  const int32_t lo = threadIdx.x * per, hi = min(P.F, lo + per);
+  const int32_t per = (P.F + c.g.size() - 1) / c.g.size();
+  const int32_t lo = c.g.rank() * per, hi = min(P.F, lo + per);
   int32_t cnt = 0;
   for (int32_t f = lo; f < hi; ++f) {
     const int32_t kind = fkind[f];
@@ -832,18 +908,18 @@ __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
     fflag[f] = ev;
     cnt += ev != 0;
   }
-  const int32_t any = __syncthreads_count(cnt);
+  const int32_t any = g_count(c, cnt);
   int32_t total = 0;
   if (any) {                                        // ordered compaction of the events
-    int32_t pos = block_scan_i32(cnt, red, ph, &total);
+    int32_t pos = g_scan(c, cnt, red, ph, &total);
     for (int32_t f = lo; f < hi && cnt; ++f)
       if (fflag[f]) { v.fList[pos++] = f; --cnt; }
   }
   const int32_t need_pass = total > 0 || v.h[H_QLEN] > 0;
-  __syncthreads();
+  c.g.sync();
   if (!need_pass) return;
   // B3: apply in the paper's order (steps 2, 3, 4), thread 0
-  if (threadIdx.x == 0 && total > 0) {
+  if (c.g.leader() && total > 0) {
     acc.z->st[S_EVENT] += total;
     for (int32_t e = 0; e < total; ++e) {     // step 2: departures
       const int32_t f = v.fList[e];
@@ -873,19 +949,21 @@ __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
       else for (int32_t j = 0; j < P.min_inst && !v.h[H_ERR]; ++j) enqueue(c, f, 1);
     }
   }
-  __syncthreads();
+  c.g.sync();
   if (v.h[H_ERR]) return;
   placement_pass(c, red, ph, t, acc);             // step 5
-  __syncthreads();
+  c.g.sync();
 }
 
 // ---------------------------------------------------------------------------- kernels
 
-// One scenario for one call (scale_step: n_req < 0; place_batch: n_req >= 0).
+// One scenario for one call (scale_step: n_req < 0; place_batch: n_req >= 0), run by a
+// group of K CTAs (K = 1: the calling CTA; K > 1: the calling cluster, crank = CTA rank).
 template <bool SMEM>
 __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem, int32_t sc, int32_t t0,
                              int32_t n_slots, int32_t n_req, const int32_t* req_scn,
-                             const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid) {
+                             const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid,
+                             int K = 1, int crank = 0) {
   uint8_t* gblock = P.state + (size_t)sc * P.L.bytes;
   uint8_t* hot = gblock;
   if (SMEM) {
@@ -900,6 +978,18 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
   }
   Scn c{sv};
   c.P = &P;
+  c.g.K = K;
+  c.g.crank = crank;
+  c.g.cph = 0;
+  c.g.gu = P.gscratch + (size_t)sc * GSCR;
+  c.g.gi = reinterpret_cast<int32_t*>(c.g.gu + 32);
+  if (K == 1) {
+    c.members = red.members;
+    c.flag = &red.flag;
+  } else {
+    c.members = reinterpret_cast<int32_t*>(c.g.gu + 48);
+    c.flag = reinterpret_cast<int32_t*>(c.g.gu + 80);
+  }
   c.frow = P.funcs + (size_t)sc * P.F * 16;
   c.scn_id = P.scen[sc * 4 + 0];
   c.om = P.scen[sc * 4 + 1];
@@ -910,11 +1000,11 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
   int ph = 0;
   View& v = c.v;
   __syncthreads();
-  if (v.h[H_ERR]) return;
+  if (v.h[H_ERR]) return;     // uniform: nobody has written since the group started
 
   if (n_req >= 0) {
     // ---- dilu_place_batch: enqueue this scenario's requests in array order, one pass
-    if (threadIdx.x == 0) {
+    if (c.g.leader()) {
       for (int32_t j = 0; j < n_req && !v.h[H_ERR]; ++j) {
         if (req_scn[j] != sc) continue;
         const int32_t f = req_func[j];
@@ -922,10 +1012,10 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
         out_iid[j] = enqueue(c, f, v.fKind[f] == K_TRAIN ? v.fNw[f] : 1);
       }
     }
-    __syncthreads();
+    c.g.sync();
     if (!v.h[H_ERR]) placement_pass(c, red, ph, t0, acc);
-    __syncthreads();
-    for (int32_t j = threadIdx.x; j < n_req; j += blockDim.x) {
+    c.g.sync();
+    for (int32_t j = c.g.rank(); j < n_req; j += c.g.size()) {
       if (req_scn[j] != sc) continue;
       const int32_t id = out_iid[j];
       int32_t g = -1;
@@ -937,17 +1027,17 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
     // ---- dilu_scale_step: the slot loop
     for (int32_t t = t0; t < t0 + n_slots; ++t) {
       if (t % P.SPS == 0) {
-        __syncthreads();                    // P2(t-1) done before state mutates
+        c.g.sync();                         // P2(t-1) done before state mutates
         boundary(c, red, ph, t, acc);
         if (v.h[H_ERR]) break;
       }
       if (v.h[H_DIRTY]) {
-        __syncthreads();
+        c.g.sync();
         rebuild_layout(c);
-        if (threadIdx.x == 0) acc.z->st[S_LAYOUT] += 1;
+        if (c.g.leader()) acc.z->st[S_LAYOUT] += 1;
       }
       phase0(c, t, acc);
-      if (threadIdx.x == 0) {
+      if (c.g.leader()) {
         const long long na = v.h[H_NACT];
         acc.z->act += na;
         acc.z->memu += na * P.M - v.h[H_SUMU];
@@ -955,15 +1045,15 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
         acc.z->maxa = na > acc.z->maxa ? na : acc.z->maxa;
         acc.z->st[S_SLOT] += 1;
       }
-      __syncthreads();
+      c.g.sync();
       phase1(c, t, acc);
-      __syncthreads();
+      c.g.sync();
       phase2(c, t, acc);
     }
   }
-  __syncthreads();
+  c.g.sync();
 
-  // ---- block-reduce the tallies once per call
+  // ---- block-reduce the tallies once per call; cluster CTAs merge with atomics
   {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     long long vals[9] = {acc.rtot, acc.rsrv, acc.rvio, acc.iexe, acc.tprg, acc.etot,
@@ -980,28 +1070,29 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
       for (int q = 0; q < 9; ++q)
         for (int k = 0; k < nw; ++k)
           s7[q] = (long long)((unsigned long long)s7[q] + (unsigned long long)red.acc[q][k]);
-      long long* T = reinterpret_cast<long long*>(P.tally) + (size_t)sc * NT;
-      T[T_ACT] += acc.z->act;
-      T[T_SMU] += acc.z->act * P.T_slot - s7[5];
-      T[T_MEMU] += acc.z->memu;
-      T[T_RTOT] += s7[0];
-      T[T_RSRV] += s7[1];
-      T[T_RVIO] += s7[2];
-      T[T_IEXE] += s7[3];
-      T[T_TPRG] += s7[4];
-      T[T_POK] += acc.z->pok;
-      T[T_PFAIL] += acc.z->pfail;
-      T[T_COLD] += acc.z->cold;
-      T[T_SOUT] += acc.z->sout;
-      T[T_SIN] += acc.z->sin;
-      T[T_SPLIT] += acc.z->split;
-      T[T_HASH] = (long long)((unsigned long long)T[T_HASH] + (unsigned long long)s7[6]);
-      T[T_ROWS] += acc.z->rows;
-      if (acc.z->maxa > T[T_MAXA]) T[T_MAXA] = acc.z->maxa;
-      long long* ST = reinterpret_cast<long long*>(P.stats) + (size_t)sc * NSTAT;
+      long long d[NT];
+      d[T_ACT] = acc.z->act;
+      d[T_SMU] = acc.z->act * P.T_slot - s7[5];
+      d[T_MEMU] = acc.z->memu;
+      d[T_RTOT] = s7[0]; d[T_RSRV] = s7[1]; d[T_RVIO] = s7[2]; d[T_IEXE] = s7[3]; d[T_TPRG] = s7[4];
+      d[T_POK] = acc.z->pok; d[T_PFAIL] = acc.z->pfail; d[T_COLD] = acc.z->cold;
+      d[T_SOUT] = acc.z->sout; d[T_SIN] = acc.z->sin; d[T_SPLIT] = acc.z->split;
+      d[T_HASH] = s7[6]; d[T_ROWS] = acc.z->rows; d[T_MAXA] = acc.z->maxa;
       acc.z->st[S_RES] += s7[7];
       acc.z->st[S_FUN] += s7[8];
-      for (int k = 0; k < NSTAT; ++k) ST[k] += acc.z->st[k];
+      unsigned long long* T = reinterpret_cast<unsigned long long*>(P.tally) + (size_t)sc * NT;
+      unsigned long long* ST = reinterpret_cast<unsigned long long*>(P.stats) + (size_t)sc * NSTAT;
+      if (K == 1) {
+        for (int k = 0; k < NT; ++k)
+          if (k != T_MAXA) T[k] += (unsigned long long)d[k];
+        if ((unsigned long long)d[T_MAXA] > T[T_MAXA]) T[T_MAXA] = (unsigned long long)d[T_MAXA];
+        for (int k = 0; k < NSTAT; ++k) ST[k] += (unsigned long long)acc.z->st[k];
+      } else {
+        for (int k = 0; k < NT; ++k)
+          if (k != T_MAXA) atomicAdd(T + k, (unsigned long long)d[k]);
+        atomicMax(T + T_MAXA, (unsigned long long)d[T_MAXA]);
+        for (int k = 0; k < NSTAT; ++k) atomicAdd(ST + k, (unsigned long long)acc.z->st[k]);
+      }
     }
   }
   if (SMEM) {
@@ -1010,11 +1101,9 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
     int4* dst = reinterpret_cast<int4*>(gblock);
     for (size_t k = threadIdx.x; k < P.L.hot_bytes / 16; k += blockDim.x) dst[k] = src[k];
   }
-  __syncthreads();
+  c.g.sync();
 }
 
-// Persistent CTAs: each pulls the next scenario from an atomic counter (zeroed by the
-// host before the launch), so long scenarios do not leave SMs idle at the tail.
 #ifndef DILU_MINB
 #define DILU_MINB 3
 #endif
@@ -1039,6 +1128,26 @@ k_run(Params Pin, int32_t* next_scn, int32_t t0,
     if (sc >= sP.S) break;
     run_scenario<SMEM>(sP, red, sv, smem, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu, out_iid);
   }
+}
+
+// Large scenarios (C3/C5): one thread-block cluster of K CTAs per scenario (cluster
+// dims set at launch, K <= 16), state in HBM/L2; clusters beyond the resident capacity
+// run in waves.  Same device code as k_run through the group abstraction.
+__global__ void __launch_bounds__(1024, 1)
+k_run_cluster(Params Pin, int32_t t0, int32_t n_slots, int32_t n_req, const int32_t* req_scn,
+              const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid) {
+  __shared__ Red red;
+  __shared__ Params sP;
+  __shared__ View sv;
+  unsigned int crank, csize;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
+  if (threadIdx.x == 0) sP = Pin;
+  __syncthreads();
+  const int32_t sc = blockIdx.x / csize;
+  if (sc >= sP.S) return;   // whole clusters only: uniform across the cluster
+  run_scenario<false>(sP, red, sv, nullptr, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu,
+                      out_iid, (int)csize, (int)crank);
 }
 
 // Initialise every scenario's block at slot 0 (one CTA per scenario).

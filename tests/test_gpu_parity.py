@@ -114,7 +114,7 @@ def test_launch_shape_invariance(mode, monkeypatch):
     run_pair(wl, [1, 599], id_cap=2048)
 
 
-@pytest.mark.parametrize("engine", ["cta", "lanes"])
+@pytest.mark.parametrize("engine", ["cta", "lanes", "cluster"])
 def test_engines_on_c1_c2(engine, monkeypatch):
     monkeypatch.setenv("DILU_ENGINE", engine)
     run_pair(di.c1(), [1, 39, 1, 59], id_cap=16)
