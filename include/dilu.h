@@ -155,11 +155,12 @@ dilu_status dilu_metrics(dilu_sim* s, int64_t* per_scenario, int64_t* sum);
  * Synchronises the stream. */
 dilu_status dilu_snapshot(dilu_sim* s, int32_t id_cap, int32_t* d_gpu, int32_t* d_inst);
 
-/* Diagnostics (tracing; off the timed path): per-scenario int64 [n_scenarios][8] (may
- * be NULL) and their sum [8] (may be NULL) of kernel counters accumulated since the
+/* Diagnostics (tracing; off the timed path): per-scenario int64 [n_scenarios][24] (may
+ * be NULL) and their sum [24] (may be NULL) of kernel counters accumulated since the
  * last create/reset: full placement attempts, retry-skip checks, row repacks, boundary
  * events, queue scans, slots simulated, warm resident-slots allocated, inference
- * function-slots dispatched.  Host or device pointers.
+ * function-slots dispatched, then 16 per-phase cycle timers (leader thread; nonzero only
+ * in a -DDILU_PHASE_TIMING build).  Host or device pointers.
  * Synchronises the stream. */
 dilu_status dilu_kernel_stats(dilu_sim* s, int64_t* per_scenario, int64_t* sum);
 

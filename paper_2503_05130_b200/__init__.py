@@ -160,11 +160,14 @@ class DiluSim:
         return gpu, inst[:, :id_cap]
 
     STAT_NAMES = ["attempts", "retry_checks", "row_repacks", "boundary_events", "queue_scans",
-                  "slots", "resident_slots", "function_slots"]
+                  "slots", "resident_slots", "function_slots", "cyc_pre_boundary", "cyc_boundary",
+                  "cyc_repack", "cyc_p0", "cyc_p1", "cyc_p2", "cyc_b3", "cyc_terminate",
+                  "cyc_enqueue", "cyc_next_attempt", "cyc_place", "t19", "t20", "t21", "t22", "t23"]
 
     def kernel_stats(self):
-        """Diagnostics: dict of summed kernel counters (dilu_kernel_stats)."""
-        tot = np.zeros(8, dtype=np.int64)
+        """Diagnostics: dict of summed kernel counters (dilu_kernel_stats); the cyc_*
+        phase timers are filled only by a -DDILU_PHASE_TIMING build."""
+        tot = np.zeros(24, dtype=np.int64)
         self._check(lib().dilu_kernel_stats(self.h, None, tot.ctypes.data))
         return dict(zip(self.STAT_NAMES, tot.tolist()))
 

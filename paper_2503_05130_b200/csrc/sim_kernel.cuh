@@ -160,6 +160,7 @@ struct Scn {
   Grp g;
   int32_t* members;          // gang member slots of the request being placed (group-visible)
   int32_t* flag;             // group-visible broadcast word
+  Acc0* z;                   // leader tallies (shared)
   const int32_t* frow;       // this scenario's input function rows [F][16]
   int32_t scn_id, om, ga;
 };
@@ -282,7 +283,20 @@ __device__ void release(Scn& c, int32_t s) {
 }
 
 // terminate a live instance (placed or pending); frees its slot
+#ifdef DILU_PHASE_TIMING
+#define TSTART long long _t0 = clock64()
+#define TSTOP(k) do { if (c.g.leader()) c.z->st[k] += clock64() - _t0; } while (0)
+#else
+#define TSTART do { } while (0)
+#define TSTOP(k) do { } while (0)
+#endif
+__device__ void terminate_impl(Scn& c, int32_t s);
 __device__ void terminate(Scn& c, int32_t s) {
+  TSTART;
+  terminate_impl(c, s);
+  TSTOP(15);
+}
+__device__ void terminate_impl(Scn& c, int32_t s) {
   View& v = c.v;
   const int32_t f = v.iFunc[s];
   if (st_of(v.iMeta[s]) == ST_PLACED) {
@@ -311,6 +325,8 @@ __device__ void compact_queue(View& v) {
     if (v.qN[q] == 0) continue;
     if (k != q) {
       v.qFunc[k] = v.qFunc[q]; v.qFirst[k] = v.qFirst[q]; v.qN[k] = v.qN[q]; v.qFail[k] = v.qFail[q];
+      v.qSlot[k] = v.qSlot[q];
+      v.iQ[v.qSlot[k]] = k;
     }
     ++k;
   }
@@ -318,17 +334,27 @@ __device__ void compact_queue(View& v) {
 }
 
 // enqueue one request of n new instances of f; returns first id or -1 on capacity error
+__device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n);
 __device__ int32_t enqueue(Scn& c, int32_t f, int32_t n) {
+  TSTART;
+  const int32_t r = enqueue_impl(c, f, n);
+  TSTOP(16);
+  return r;
+}
+__device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
   View& v = c.v;
   if (v.h[H_FSTOP] < n) { v.h[H_ERR] = 6; return -1; }
   if (v.h[H_QLEN] == c.P->I) compact_queue(v);
   const int32_t first = v.h[H_NEXT_IID];
+  const int32_t q = v.h[H_QLEN]++;
   for (int32_t j = 0; j < n; ++j) {
     const int32_t s = v.fstack[--v.h[H_FSTOP]];
     v.iId[s] = v.h[H_NEXT_IID]++;
     v.iFunc[s] = f;
     v.iMeta[s] = ST_PEND;
     v.iReady[s] = 0;
+    v.iQ[s] = q;                      // request index (single-instance kills are O(1))
+    if (j == 0) v.qSlot[q] = s;
     for (int k = 0; k < MAXST; ++k) { v.iG[s * MAXST + k] = -1; v.iShare[s * MAXST + k] = 0; }
     v.iBmin[s] = BIG;
     v.iBmin[c.P->I + s] = BIG;
@@ -336,7 +362,6 @@ __device__ int32_t enqueue(Scn& c, int32_t f, int32_t n) {
     v.fNlive[f] += 1;
     v.h[H_NLIVE] += 1;
   }
-  const int32_t q = v.h[H_QLEN]++;
   v.qFunc[q] = f; v.qFirst[q] = first; v.qN[q] = n; v.qFail[q] = -1;
   return first;
 }
@@ -532,11 +557,13 @@ __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
   bool removed = false;
   int32_t q = 0;
   for (;;) {
+    TSTART;
     if (c.g.lead_warp()) {
       const int32_t e = next_attempt(c, q, qn, acc);
       if (threadIdx.x == 0) *c.flag = e;
     }
     c.g.sync();
+    TSTOP(17);
     q = c.g.K == 1 ? *c.flag : __ldcg(c.flag);
     if (q >= qn) break;
     const int32_t n = v.qN[q];
@@ -551,9 +578,13 @@ __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
     }
     c.g.sync();
     int placed = 0;
-    for (int j = 0; j < n; ++j) {
-      if (!place_one(c, red, ph, c.g.K == 1 ? c.members[j] : __ldcg(c.members + j))) break;
-      ++placed;
+    {
+      TSTART;
+      for (int j = 0; j < n; ++j) {
+        if (!place_one(c, red, ph, c.g.K == 1 ? c.members[j] : __ldcg(c.members + j))) break;
+        ++placed;
+      }
+      TSTOP(18);
     }
     if (c.g.leader()) {
       for (int j = 0; j < placed; ++j) {   // clear I* marks
@@ -631,7 +662,7 @@ __device__ void rebuild_layout(Scn& c) {
 // P0: arrivals and even dispatch over warm instances (Q16, Q17).
 // A_f(t) = (pat[p_f][(t + phase_f) mod T_pat] * scale_f) >> 10; the pattern index is
 // advanced incrementally (set at registration), so no modulo runs per slot.
-__device__ void phase0(Scn& c, int32_t t, Acc& acc) {
+__device__ void phase0(Scn& c, int32_t t, Acc& acc, int32_t pf_f, long long pf_x) {
   View& v = c.v;
   const Params& P = *c.P;
   const int32_t* __restrict__ infl = v.fInfL;
@@ -652,7 +683,9 @@ __device__ void phase0(Scn& c, int32_t t, Acc& acc) {
     if (!reg[f]) continue;
     const int32_t idx = pidx[f];
     pidx[f] = idx + 1 == Tp ? 0 : idx + 1;
-    const long long x = __ldg(gpat + (size_t)fpat[f] * Tp + idx);
+    // the first item's pattern value was prefetched at slot start (valid unless f was
+    // registered at this boundary: pf_f is only set for functions registered before it)
+    const long long x = f == pf_f ? pf_x : __ldg(gpat + (size_t)fpat[f] * Tp + idx);
     const int32_t A = (int32_t)((x * fscale[f]) >> 10);
     acc.nfun += 1;
     facc[f] += A;
@@ -811,10 +844,11 @@ __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
       }
     } else {
       for (int32_t s = lh[f]; s >= 0; s = nxt[s]) {
+        const int32_t nst = nst_of(meta[s]);
+        if (nst <= 1) continue;                 // unsplit: finished in P1
         const int32_t b = bmin[s];
         if (b == BIG) continue;
         bmin[s] = BIG;
-        const int32_t nst = nst_of(meta[s]);
         const int32_t ibs = v.fIbs[f];
         const int32_t cst = (v.fCb[f] + nst - 1) / nst;
         const int32_t rr = r[s];
@@ -917,7 +951,16 @@ __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
   }
   const int32_t need_pass = total > 0 || v.h[H_QLEN] > 0;
   c.g.sync();
-  if (!need_pass) return;
+#ifdef DILU_PHASE_TIMING
+  long long bt0 = clock64();
+  if (c.g.leader()) acc.z->st[14] -= bt0;   // st[14] += (end of B3) - (end of B1)
+#endif
+  if (!need_pass) {
+#ifdef DILU_PHASE_TIMING
+    if (c.g.leader()) acc.z->st[14] += bt0;
+#endif
+    return;
+  }
   // B3: apply in the paper's order (steps 2, 3, 4), thread 0
   if (c.g.leader() && total > 0) {
     acc.z->st[S_EVENT] += total;
@@ -936,7 +979,7 @@ __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
         acc.z->sout += 1;
       } else if (ev & EV_IN) {
         const int32_t victim = v.fLt[f];        // highest live id (Q19)
-        if (st_of(v.iMeta[victim]) == ST_PEND) kill_queue_entry_with_id(v, v.iId[victim]);
+        if (st_of(v.iMeta[victim]) == ST_PEND) v.qN[v.iQ[victim]] = 0;   // its own request
         terminate(c, victim);
         acc.z->sin += 1;
       }
@@ -950,6 +993,9 @@ __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
     }
   }
   c.g.sync();
+#ifdef DILU_PHASE_TIMING
+  if (c.g.leader()) acc.z->st[14] += clock64();
+#endif
   if (v.h[H_ERR]) return;
   placement_pass(c, red, ph, t, acc);             // step 5
   c.g.sync();
@@ -996,6 +1042,7 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
   c.ga = P.scen[sc * 4 + 2];
   Acc acc = {};
   acc.z = &red.z;
+  c.z = &red.z;
   if (threadIdx.x == 0) red.z = Acc0{};
   int ph = 0;
   View& v = c.v;
@@ -1026,9 +1073,26 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
   } else {
     // ---- dilu_scale_step: the slot loop
     for (int32_t t = t0; t < t0 + n_slots; ++t) {
+#ifdef DILU_PHASE_TIMING
+      long long tk0 = clock64(), tk1;
+#define TICK(slot) do { tk1 = clock64(); if (c.g.leader()) acc.z->st[8 + (slot)] += tk1 - tk0; tk0 = tk1; } while (0)
+#else
+#define TICK(slot) do { } while (0)
+#endif
+      int32_t pf_f = -1;                    // prefetch this thread's first P0 pattern value
+      long long pf_x = 0;
+      {
+        const int32_t k = c.g.rank();
+        if (k < v.h[H_NINF]) {
+          const int32_t f = v.fInfL[k];
+          if (v.fReg[f]) { pf_f = f; pf_x = __ldg(P.pat + (size_t)v.fPat[f] * P.Tp + v.fPidx[f]); }
+        }
+      }
       if (t % P.SPS == 0) {
         c.g.sync();                         // P2(t-1) done before state mutates
+        TICK(0);
         boundary(c, red, ph, t, acc);
+        TICK(1);
         if (v.h[H_ERR]) break;
       }
       if (v.h[H_DIRTY]) {
@@ -1036,7 +1100,8 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
         rebuild_layout(c);
         if (c.g.leader()) acc.z->st[S_LAYOUT] += 1;
       }
-      phase0(c, t, acc);
+      TICK(2);
+      phase0(c, t, acc, pf_f, pf_x);
       if (c.g.leader()) {
         const long long na = v.h[H_NACT];
         acc.z->act += na;
@@ -1046,9 +1111,13 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
         acc.z->st[S_SLOT] += 1;
       }
       c.g.sync();
+      TICK(3);
       phase1(c, t, acc);
       c.g.sync();
+      TICK(4);
       phase2(c, t, acc);
+      TICK(5);
+#undef TICK
     }
   }
   c.g.sync();

@@ -19,7 +19,7 @@ constexpr int MAXST = 4;   // LLM pipeline stages
 constexpr int NT = 17;     // tally vector length
 constexpr int32_t BIG = 0x7fffffff;
 constexpr int RLOG = 64;   // release log ring (GPU, epoch) for the placement retry skip
-constexpr int NSTAT = 8;   // kernel statistics per scenario (dilu_kernel_stats)
+constexpr int NSTAT = 24;  // kernel statistics per scenario (dilu_kernel_stats): 8 counters + 16 timers
 
 enum : int32_t { K_UNUSED = -1, K_INF = 0, K_LLM = 1, K_TRAIN = 2 };
 enum : int32_t { ST_FREE = 0, ST_PEND = 1, ST_PLACED = 2 };
@@ -47,7 +47,7 @@ struct Layout {
       fPhase, fCap1;
   size_t fReg, fNsamp, fAcc, fHead, fUp, fDown, fThrn, fNlive, fLh, fLt, fGang, fFlag, fK,
       fList, fArr, fDep, fPidx, fInfL, fDefL;
-  size_t qFunc, qFirst, qN, qFail;
+  size_t qFunc, qFirst, qN, qFail, qSlot, iQ;
   size_t hot_bytes, bytes;
 };
 
@@ -77,15 +77,16 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W) {
   L.fGang = take(4 * 2 * (size_t)F); L.fFlag = take(4 * (size_t)F);
   L.fArr = take(4 * (size_t)F); L.fDep = take(4 * (size_t)F); L.fPidx = take(4 * (size_t)F);
   L.fInfL = take(4 * (size_t)F); L.fDefL = take(4 * (size_t)F);
-  L.hot_bytes = align16(o);
-  // cold region: touched on placement/release/scaling events only -> stays in HBM/L2
-  L.gRel = take(4 * (size_t)G);
-  L.iG = take(4 * (size_t)I * MAXST); L.iShare = take(4 * (size_t)I * MAXST);
-  L.iBmin = take(4 * 2 * (size_t)I); L.fstack = take(4 * (size_t)I);
+  // serial-path structures the leader walks every boundary (queue, free stack, ...)
+  L.gRel = take(4 * (size_t)G); L.fstack = take(4 * (size_t)I);
   L.fPrio = take(4 * (size_t)F); L.fCold = take(4 * (size_t)F); L.fLt = take(4 * (size_t)F);
   L.fK = take(4 * (size_t)F); L.fList = take(4 * (size_t)F);
   L.qFunc = take(4 * (size_t)I); L.qFirst = take(4 * (size_t)I); L.qN = take(4 * (size_t)I);
-  L.qFail = take(4 * (size_t)I);
+  L.qFail = take(4 * (size_t)I); L.qSlot = take(4 * (size_t)I); L.iQ = take(4 * (size_t)I);
+  L.hot_bytes = align16(o);
+  // cold region: stage placements and LLM stage minima -> stays in HBM/L2
+  L.iG = take(4 * (size_t)I * MAXST); L.iShare = take(4 * (size_t)I * MAXST);
+  L.iBmin = take(4 * 2 * (size_t)I);
   L.bytes = align16(o);
   return L;
 }
@@ -100,7 +101,7 @@ struct View {
   int64_t* fCap1;
   int32_t *fReg, *fNsamp, *fAcc, *fHead, *fUp, *fDown, *fThrn, *fNlive, *fLh, *fLt, *fGang,
       *fFlag, *fK, *fList, *fArr, *fDep, *fPidx, *fInfL, *fDefL;
-  int32_t *qFunc, *qFirst, *qN, *qFail;
+  int32_t *qFunc, *qFirst, *qN, *qFail, *qSlot, *iQ;
   int32_t* ring;  // global [F][W]
 };
 
@@ -121,7 +122,7 @@ inline View make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
   P32(fReg); P32(fNsamp); P32(fAcc); P32(fHead); P32(fUp); P32(fDown); P32(fThrn); P32(fNlive);
   P32(fLh); P32(fLt); P32(fGang); P32(fFlag); P32(fK); P32(fList); P32(fArr); P32(fDep);
   P32(fPidx); P32(fInfL); P32(fDefL);
-  P32(qFunc); P32(qFirst); P32(qN); P32(qFail);
+  P32(qFunc); P32(qFirst); P32(qN); P32(qFail); P32(qSlot); P32(iQ);
 #undef P32
   v.ring = nullptr;
   return v;
