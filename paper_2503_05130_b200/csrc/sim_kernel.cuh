@@ -554,29 +554,59 @@ __device__ int32_t next_attempt(Scn& c, int32_t q, int32_t qn, Acc& acc) {
 __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
   View& v = c.v;
   const int32_t qn = v.h[H_QLEN];
-  bool removed = false;
-  int32_t q = 0;
+  bool removed = false;                 // leader only
+  int32_t q = 0, prev = -1, prev_placed = 0;
   for (;;) {
+    // One warp-0 section per attempt: finish the previous request (leader), find the next
+    // request needing a real attempt (warp 0, 32 entries per step), gather its members
+    // (leader); then a single group barrier.
     TSTART;
     if (c.g.lead_warp()) {
+      if (c.g.leader() && prev >= 0) {
+        const int32_t n = v.qN[prev], f = v.qFunc[prev];
+        for (int j = 0; j < prev_placed; ++j) {   // clear I* marks
+          const int32_t s = c.members[j];
+          const int ns = nst_of(v.iMeta[s]);
+          for (int k = 0; k < ns; ++k) v.gExcl[v.iG[s * MAXST + k]] = 0;
+        }
+        if (prev_placed == n) {
+          const int32_t cold = v.fCold[f];
+          for (int j = 0; j < n; ++j) {
+            const int32_t s = c.members[j];
+            v.iMeta[s] = (v.iMeta[s] & ~3) | ST_PLACED;
+            v.iReady[s] = t + cold;
+            acc.z->pok += 1;
+            if (is_inf(v.fKind[f]) && cold > 0) acc.z->cold += 1;
+            if (nst_of(v.iMeta[s]) > 1) acc.z->split += 1;
+          }
+          v.qN[prev] = 0;
+          removed = true;
+        } else {
+          for (int j = 0; j < prev_placed; ++j) release(c, c.members[j]);  // rollback
+          acc.z->pfail += 1;
+          v.qFail[prev] = v.h[H_EPOCH];
+        }
+      }
+      __syncwarp();
       const int32_t e = next_attempt(c, q, qn, acc);
-      if (threadIdx.x == 0) *c.flag = e;
+      if (c.g.leader()) {
+        *c.flag = e;
+        if (e < qn) {                   // gang members, ascending id
+          const int32_t n = v.qN[e], f = v.qFunc[e], first = v.qFirst[e];
+          int j = 0;
+          for (int32_t s = v.fLh[f]; s >= 0 && j < n; s = v.iNext[s]) {
+            const int32_t id = v.iId[s];
+            if (id >= first && id < first + n) c.members[j++] = s;
+          }
+          acc.z->st[S_ATTEMPT] += 1;
+        }
+      }
     }
     c.g.sync();
     TSTOP(17);
     q = c.g.K == 1 ? *c.flag : __ldcg(c.flag);
     if (q >= qn) break;
     const int32_t n = v.qN[q];
-    const int32_t f = v.qFunc[q], first = v.qFirst[q];
-    if (c.g.leader()) {              // gang members, ascending id
-      int j = 0;
-      for (int32_t s = v.fLh[f]; s >= 0 && j < n; s = v.iNext[s]) {
-        const int32_t id = v.iId[s];
-        if (id >= first && id < first + n) c.members[j++] = s;
-      }
-      acc.z->st[S_ATTEMPT] += 1;
-    }
-    c.g.sync();
     int placed = 0;
     {
       TSTART;
@@ -586,31 +616,8 @@ __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
       }
       TSTOP(18);
     }
-    if (c.g.leader()) {
-      for (int j = 0; j < placed; ++j) {   // clear I* marks
-        const int32_t s = c.members[j];
-        const int ns = nst_of(v.iMeta[s]);
-        for (int k = 0; k < ns; ++k) v.gExcl[v.iG[s * MAXST + k]] = 0;
-      }
-      if (placed == n) {
-        const int32_t cold = v.fCold[f];
-        for (int j = 0; j < n; ++j) {
-          const int32_t s = c.members[j];
-          v.iMeta[s] = (v.iMeta[s] & ~3) | ST_PLACED;
-          v.iReady[s] = t + cold;
-          acc.z->pok += 1;
-          if (is_inf(v.fKind[f]) && cold > 0) acc.z->cold += 1;
-          if (nst_of(v.iMeta[s]) > 1) acc.z->split += 1;
-        }
-        v.qN[q] = 0;
-        removed = true;
-      } else {
-        for (int j = 0; j < placed; ++j) release(c, c.members[j]);  // rollback
-        acc.z->pfail += 1;
-        v.qFail[q] = v.h[H_EPOCH];
-      }
-    }
-    c.g.sync();
+    prev = q;
+    prev_placed = placed;
     ++q;
   }
   if (c.g.leader() && removed) compact_queue(v);
