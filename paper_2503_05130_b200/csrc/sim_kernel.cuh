@@ -249,8 +249,9 @@ __device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
   v.gN[g] += 1;
   const int32_t meta = v.iMeta[s];
   const int k0 = nst_of(meta);
-  v.iG[s * MAXST + k0] = g;
+  v.iG[s * MAXST + k0] = (int16_t)g;
   v.iShare[s * MAXST + k0] = share;
+  if (k0 == 0) v.iSh0[s] = share;
   v.iMeta[s] = (meta & ~(7 << 4)) | ((k0 + 1) << 4);
   v.gExcl[g] = 1;             // I* of the request in flight (Q7)
   v.h[H_DIRTY] = 1;
@@ -263,7 +264,7 @@ __device__ void release(Scn& c, int32_t s) {
   const int n = nst_of(meta);
   for (int k = 0; k < n; ++k) {
     const int32_t g = v.iG[s * MAXST + k];
-    const int32_t sh = v.iShare[s * MAXST + k];
+    const int32_t sh = k == 0 ? v.iSh0[s] : v.iShare[s * MAXST + k];
     v.gR[g] -= v.fReq[f];
     v.gL[g] -= v.fLim[f];
     v.gU[g] -= sh;
@@ -276,7 +277,6 @@ __device__ void release(Scn& c, int32_t s) {
     v.gN[g] = nr - 1;
     if (nr - 1 == 0) v.h[H_NACT] -= 1;
     v.iG[s * MAXST + k] = -1;
-    v.iShare[s * MAXST + k] = 0;
   }
   v.iMeta[s] = meta & ~(7 << 4);
   v.h[H_DIRTY] = 1;
@@ -355,7 +355,7 @@ __device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
     v.iReady[s] = 0;
     v.iQ[s] = q;                      // request index (single-instance kills are O(1))
     if (j == 0) v.qSlot[q] = s;
-    for (int k = 0; k < MAXST; ++k) { v.iG[s * MAXST + k] = -1; v.iShare[s * MAXST + k] = 0; }
+    for (int k = 0; k < MAXST; ++k) v.iG[s * MAXST + k] = -1;
     v.iBmin[s] = BIG;
     v.iBmin[c.P->I + s] = BIG;
     list_append(v, f, s);
@@ -875,7 +875,7 @@ __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
 
 enum : int32_t { EV_DEP = 1, EV_OUT = 2, EV_IN = 4, EV_ARR = 8 };
 
-__device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
+__device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, int32_t pf_ring) {
   View& v = c.v;
   const Params& P = *c.P;
   const int32_t sec = t / P.SPS;
@@ -915,7 +915,10 @@ __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
           if (thr >= 0) {
             const long long cu = (long long)thr * cap1, cd = (long long)(thr - 1) * cap1;
             int32_t du = val > cu, dd = val < cd;
-            if (ns >= W) { const int32_t old = ring[head]; du -= old > cu; dd -= old < cd; }
+            if (ns >= W) {
+              const int32_t old = f == lo ? pf_ring : ring[head];   // prefetched at slot start
+              du -= old > cu; dd -= old < cd;
+            }
             fup[f] += du;
             fdown[f] += dd;
           }
@@ -1088,6 +1091,12 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
 #endif
       int32_t pf_f = -1;                    // prefetch this thread's first P0 pattern value
       long long pf_x = 0;
+      int32_t pf_ring = 0;                  // ... and, at a boundary, its first B1 ring word
+      if (t % P.SPS == 0) {
+        const int32_t per = (P.F + c.g.size() - 1) / c.g.size();
+        const int32_t f0 = c.g.rank() * per;
+        if (f0 < P.F && v.fReg[f0]) pf_ring = v.ring[(size_t)f0 * P.W + v.fHead[f0]];
+      }
       {
         const int32_t k = c.g.rank();
         if (k < v.h[H_NINF]) {
@@ -1098,7 +1107,7 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
       if (t % P.SPS == 0) {
         c.g.sync();                         // P2(t-1) done before state mutates
         TICK(0);
-        boundary(c, red, ph, t, acc);
+        boundary(c, red, ph, t, acc, pf_ring);
         TICK(1);
         if (v.h[H_ERR]) break;
       }
@@ -1243,6 +1252,7 @@ __global__ void k_init(Params P) {
   for (int32_t s = threadIdx.x; s < P.I; s += blockDim.x) {
     v.iId[s] = -1; v.iFunc[s] = -1; v.iMeta[s] = ST_FREE; v.iReady[s] = 0; v.iNext[s] = -1;
     for (int k = 0; k < MAXST; ++k) { v.iG[s * MAXST + k] = -1; v.iShare[s * MAXST + k] = 0; }
+    v.iSh0[s] = 0;
     v.iR[s] = 0; v.iR[P.I + s] = 0; v.iBmin[s] = BIG; v.iBmin[P.I + s] = BIG;
     v.fstack[s] = P.I - 1 - s;
   }

@@ -42,7 +42,7 @@ struct Layout {
   // byte offsets inside one block
   size_t hdr;
   size_t gR, gL, gU, gN, gRes, gExcl, gGrow, gRel, rlG, rlE;
-  size_t iId, iFunc, iMeta, iReady, iG, iShare, iNext, iR, iBmin, fstack;
+  size_t iId, iFunc, iMeta, iReady, iG, iSh0, iShare, iNext, iR, iBmin, fstack;
   size_t fKind, fPrio, fReq, fLim, fMem, fCb, fIbs, fNw, fCold, fCls, fDtr, fPat, fScale,
       fPhase, fCap1;
   size_t fReg, fNsamp, fAcc, fHead, fUp, fDown, fThrn, fNlive, fLh, fLt, fGang, fFlag, fK,
@@ -85,7 +85,9 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W) {
   L.qFail = take(4 * (size_t)I); L.qSlot = take(4 * (size_t)I); L.iQ = take(4 * (size_t)I);
   L.hot_bytes = align16(o);
   // cold region: stage placements and LLM stage minima -> stays in HBM/L2
-  L.iG = take(4 * (size_t)I * MAXST); L.iShare = take(4 * (size_t)I * MAXST);
+  L.iG = take(2 * (size_t)I * MAXST);   // int16 stage GPUs (G <= 32767)
+  L.iSh0 = take(4 * (size_t)I);         // stage-0 memory share
+  L.iShare = take(4 * (size_t)I * MAXST);
   L.iBmin = take(4 * 2 * (size_t)I);
   L.bytes = align16(o);
   return L;
@@ -95,7 +97,8 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W) {
 struct View {
   int32_t* h;
   int32_t *gR, *gL, *gU, *gN, *gRes, *gExcl, *gGrow, *gRel, *rlG, *rlE;
-  int32_t *iId, *iFunc, *iMeta, *iReady, *iG, *iShare, *iNext, *iR, *iBmin, *fstack;
+  int32_t *iId, *iFunc, *iMeta, *iReady, *iSh0, *iShare, *iNext, *iR, *iBmin, *fstack;
+  int16_t* iG;
   int32_t *fKind, *fPrio, *fReq, *fLim, *fMem, *fCb, *fIbs, *fNw, *fCold, *fCls, *fDtr, *fPat,
       *fScale, *fPhase;
   int64_t* fCap1;
@@ -114,7 +117,8 @@ inline View make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
 #define P32(name) v.name = reinterpret_cast<int32_t*>((L.name < L.hot_bytes ? hot : b) + L.name)
   v.h = reinterpret_cast<int32_t*>(hot + L.hdr);
   P32(gR); P32(gL); P32(gU); P32(gN); P32(gRes); P32(gExcl); P32(gGrow); P32(gRel); P32(rlG); P32(rlE);
-  P32(iId); P32(iFunc); P32(iMeta); P32(iReady); P32(iG); P32(iShare); P32(iNext); P32(iR);
+  P32(iId); P32(iFunc); P32(iMeta); P32(iReady); P32(iSh0); P32(iShare); P32(iNext); P32(iR);
+  v.iG = reinterpret_cast<int16_t*>((L.iG < L.hot_bytes ? hot : b) + L.iG);
   P32(iBmin); P32(fstack);
   P32(fKind); P32(fPrio); P32(fReq); P32(fLim); P32(fMem); P32(fCb); P32(fIbs); P32(fNw);
   P32(fCold); P32(fCls); P32(fDtr); P32(fPat); P32(fScale); P32(fPhase);

@@ -185,3 +185,36 @@ def test_degenerate_inputs():
     zero = di.c2(seed=5, T=120)
     zero = di.Workload("zero", zero.cfg, zero.scen, zero.funcs, np.zeros_like(zero.patterns), 120)
     run_pair(zero, [120], id_cap=1024)
+
+
+# ------------------------------------------------------------------ full sizes
+# BASELINE.json's full sizes in the launch configuration bench.py times; the oracle
+# computes a sample of the outputs one by one (task contract).
+
+def test_c4_full_size_sampled():
+    """All 4,096 C4 scenarios for the full hour on the GPU (bench launch shape); 24
+    scenarios spread over the sweep recomputed by the oracle, per-scenario bit-exact."""
+    wl = di.c4(n_scenarios=4096)
+    gs = gpu_sim(wl)
+    gs.scale_step(wl.n_slots)
+    per, tot = gs.metrics()
+    per = per.cpu().numpy()
+    idx = np.linspace(0, 4095, 24).round().astype(int)
+    rper, _ = oracle.run(wl.subset(idx), threads=8)
+    assert np.array_equal(per[idx], rper)
+    assert tot.cpu().numpy()[T["gpu_row_slots"]] == 4096 * 64 * 3600
+
+
+def test_c5_full_size_window():
+    """One C5 scenario at full size (16,384 GPUs, ~90,500 functions, 100 ms slots, cluster
+    engine) for the first 30 s, including the initial fleet placement: full state and
+    tallies bit-exact against the oracle."""
+    wl = di.c5(n_scenarios=1, T=36000)
+    run_pair(wl, [10, 290], id_cap=160000)
+
+
+@pytest.mark.slow
+def test_c3_full_day():
+    """C3 (1,024 GPUs, 24 h at 1 s slots): every tally of the whole day."""
+    wl = di.c3(T=86400)
+    run_pair(wl, [86400], snap=False)
