@@ -5,7 +5,7 @@ allocation, no scaling rule, no capacity formula).  It only writes the integer
 input tables both sides consume:
 
 * a config row (20 int32, field order ``CONFIG_FIELDS``),
-* per-scenario rows (4 int32: global scenario id, Omega, gamma, reserved),
+* per-scenario rows (4 int32: global scenario id, Omega, gamma, baseline mode),
 * the quantised profile table (16 int32 per function row, ``FUNC_FIELDS``),
 * the per-slot arrival pattern table (int32 ``[n_patterns][pattern_len]``).
 
@@ -33,7 +33,8 @@ FUNC_FIELDS = [
     "duty_pm", "cold_slots", "affinity_class", "arrive_sec", "depart_sec",
     "pattern", "scale_q10", "phase_slots",
 ]
-SCEN_FIELDS = ["scenario_id", "omega_pm", "gamma_pm", "reserved"]
+SCEN_FIELDS = ["scenario_id", "omega_pm", "gamma_pm", "mode"]
+MODES = {"dilu": 0, "exclusive": 1, "static_limit": 2, "static_request": 3, "eager_horizontal": 4}
 FI = {n: i for i, n in enumerate(FUNC_FIELDS)}
 
 NEVER = 2**31 - 1          # depart_sec for "never departs"
@@ -385,6 +386,22 @@ def scaled(name: str, G: int, n_jobs: int, n_llm: int, n_inf: int, slot_ms: int,
     """A large-config-shaped workload at a reduced size (parity tests)."""
     return _large(name, G, n_jobs, n_llm, n_inf, slot_ms, T, seeds, T * slot_ms // 1000,
                   max_instances, 777, base_frac=0.5)
+
+
+def with_modes(wl: Workload, modes) -> Workload:
+    """The same fleet under baseline modes (SURVEY s8(f) #1): scenario i gets modes[i]."""
+    scen = wl.scen.copy()
+    scen[:, 3] = np.asarray(modes, dtype=np.int32)
+    return Workload(wl.name, wl.cfg, scen, wl.funcs, wl.patterns, wl.n_slots, wl.note)
+
+
+def replicate(wl: Workload, n: int) -> Workload:
+    """n copies of scenario 0 (for running one fleet under several modes)."""
+    cfg = dict(wl.cfg)
+    cfg["n_scenarios"] = n
+    scen = np.repeat(wl.scen[:1], n, axis=0)
+    return Workload(wl.name, cfg, scen, np.repeat(wl.funcs[:1], n, axis=0), wl.patterns,
+                    wl.n_slots, wl.note)
 
 
 def by_name(name: str, **kw) -> Workload:

@@ -89,8 +89,18 @@ typedef struct {
 typedef struct {
   int32_t scenario_id;        /* global id, feeds alloc_hash so shards sum identically     */
   int32_t omega_pm, gamma_pm;
-  int32_t reserved;
+  int32_t mode;               /* DILU_MODE_*: Dilu or a baseline      */
 } dilu_scenario;
+
+/* Baseline modes, applied per scenario to the same profile table:
+ * EXCLUSIVE: every instance on its own GPU, whole-GPU grant (pass-through);
+ * STATIC_LIMIT: MPS-l, request := limit, no spare sharing;
+ * STATIC_REQUEST: MPS-r, limit := request;
+ * EAGER_HORIZONTAL: FaST-GS+-like, MPS-l quotas and scale-out/in on the latest 1 s
+ * sample instead of the lazy 40 s window.  Limit-quota modes
+ * require limit <= Omega (DILU_E_USAGE otherwise). */
+enum { DILU_MODE_DILU = 0, DILU_MODE_EXCLUSIVE = 1, DILU_MODE_STATIC_LIMIT = 2,
+       DILU_MODE_STATIC_REQUEST = 3, DILU_MODE_EAGER_HORIZONTAL = 4 };
 
 /* One quantised profile-table row <IBS, request, limit, memory> plus lifecycle
  * (Table 1).  kind -1 marks an unused row. */

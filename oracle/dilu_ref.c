@@ -22,6 +22,7 @@
 
 enum { K_UNUSED = -1, K_INF = 0, K_LLM = 1, K_TRAIN = 2 };
 enum { ST_PENDING = 0, ST_PLACED = 1, ST_TERMINATED = 2 };
+enum { M_DILU = 0, M_EXCLUSIVE = 1, M_STATIC_LIMIT = 2, M_STATIC_REQUEST = 3, M_EAGER = 4 };
 enum {
   T_GPU_SLOTS_ACTIVE = 0, T_SM_UNUSED, T_MEM_UNUSED, T_REQ_TOTAL, T_REQ_SERVED,
   T_REQ_VIOLATED, T_INF_EXEC, T_TRAIN_PROGRESS, T_PLACEMENTS_OK, T_PLACEMENT_FAILURES,
@@ -60,7 +61,7 @@ typedef struct {
   const ref_config* cfg;
   const ref_func* fn;          /* this scenario's function rows [F]              */
   const int32_t* pat;
-  int32_t scn_id, omega_u, gamma_u;
+  int32_t scn_id, omega_u, gamma_u, mode;
   RGpu* gpu;                   /* [G] */
   RFunc* fs;                   /* [F] */
   RInst* inst;                 /* indexed by instance id */
@@ -396,16 +397,20 @@ static int32_t place_one(RScen* s, int32_t id, const int32_t* Istar, int32_t nI)
       if (s->fn[s->inst[s->gpu[g].res[j]].func].affinity_class == F->affinity_class) aff = 1;
     if (aff) wa[nwa++] = g; else other[nother++] = g;
   }
-  int32_t istar = select_opt_gpu(nwa, wa, R, L, U, nres, F->req_pm, F->lim_pm, F->mem_mib,
-                                 s->omega_u, s->gamma_u, c->mem_mib, c->q_pm, c->alpha_w, c->beta_w);
-  if (istar == -1)  /* "Select from the GPUs without WA" */
+  /* Exclusive baseline: "All GPUs are allocated exclusively to DL function instances via
+   * pass-through" -- no sharing, so only a new GPU qualifies. */
+  const int exclusive = s->mode == M_EXCLUSIVE;
+  int32_t istar = exclusive ? -1 :
+      select_opt_gpu(nwa, wa, R, L, U, nres, F->req_pm, F->lim_pm, F->mem_mib,
+                     s->omega_u, s->gamma_u, c->mem_mib, c->q_pm, c->alpha_w, c->beta_w);
+  if (istar == -1 && !exclusive)  /* "Select from the GPUs without WA" */
     istar = select_opt_gpu(nother, other, R, L, U, nres, F->req_pm, F->lim_pm, F->mem_mib,
                            s->omega_u, s->gamma_u, c->mem_mib, c->q_pm, c->alpha_w, c->beta_w);
   if (istar != -1) {
     commit(s, id, istar, F->mem_mib);
     ok = 1;
   } else {
-    if (F->kind == K_LLM && (c->flags & 1)) {  /* Principle 2 worst-fit split */
+    if (F->kind == K_LLM && (c->flags & 1) && !exclusive) {  /* Principle 2 worst-fit split */
       int32_t sg[MAX_STAGES], sh[MAX_STAGES];
       int32_t k = dilu_ref_llm_split(G, active, R, L, U, nres, excl, F->req_pm, F->lim_pm,
                                      F->mem_mib, s->omega_u, s->gamma_u, c->mem_mib,
@@ -523,11 +528,19 @@ static void boundary(RScen* s, int32_t t, int32_t sec) {
   for (int32_t f = 0; f < F; ++f) {
     RFunc* Fs = &s->fs[f];
     const ref_func* Fn = &s->fn[f];
-    if (!Fs->registered || !is_inf(Fn->kind) || Fs->nsamp < W) continue;
+    if (!Fs->registered || !is_inf(Fn->kind) || Fs->nsamp < (s->mode == M_EAGER ? 1 : W)) continue;
     int32_t k = 0;
     int64_t cap1 = dilu_ref_cap1(c->slot_ms, Fn->req_pm, Fn->work_per_batch, Fn->ibs);
-    int32_t dec = dilu_ref_scaling_decision(W, Fs->ring, Fs->nlive, cap1, c->phi_out, c->phi_in,
-                                            c->min_instances, &k);
+    int32_t dec;
+    if (s->mode == M_EAGER) {
+      /* FaST-GS+-like reactive scaling: decide on the latest one-second sample alone,
+       * i.e. the same rule with a window of 1 and phi_out = 1, phi_in = 0. */
+      int32_t last = Fs->ring[(Fs->head + W - 1) % W];
+      dec = dilu_ref_scaling_decision(1, &last, Fs->nlive, cap1, 1, 0, c->min_instances, &k);
+    } else {
+      dec = dilu_ref_scaling_decision(W, Fs->ring, Fs->nlive, cap1, c->phi_out, c->phi_in,
+                                      c->min_instances, &k);
+    }
     if (dec == 1) {
       for (int32_t j = 0; j < k; ++j) enqueue(s, f, 1);
       s->tally[T_SCALE_OUT] += 1;
@@ -582,6 +595,7 @@ static void check_invariants(RScen* s, int32_t t) {
     if (I->warm)
       for (int32_t k = 0; k < I->nst; ++k) {
         int64_t rq = (int64_t)F->req_pm * c->slot_ms, lm = (int64_t)F->lim_pm * c->slot_ms;
+        if (s->mode == M_EXCLUSIVE) lm = 1000LL * c->slot_ms;   /* pass-through ceiling */
         if (I->a[k] < rq || I->a[k] > lm)
           fail(s, REF_E_INVARIANT, "I4 violated: instance %d slot %d", id, t);
       }
@@ -637,6 +651,7 @@ static void slot(RScen* s, int32_t t) {
       stg[n] = k;
       rq[n] = (int64_t)Fn->req_pm * c->slot_ms;                  /* R3 */
       lm[n] = (int64_t)Fn->lim_pm * c->slot_ms;
+      if (s->mode == M_EXCLUSIVE) lm[n] = T_slot;               /* pass-through: whole GPU */
       if (Fn->kind == K_TRAIN) {
         d[n] = lm[n] * Fn->duty_pm / 1000;                        /* comm idle */
       } else {
@@ -753,6 +768,8 @@ static int32_t validate(const ref_config* c, const ref_scenario* scen, const ref
     int32_t ga = scen ? scen[sc].gamma_pm : c->gamma_pm;
     if (om < 1 || om > c->q_pm) BAD("scenario %d: omega_pm must be in [1, q_pm] (Q12)", sc);
     if (ga < om) BAD("scenario %d: gamma_pm < omega_pm (S:242)", sc);
+    const int32_t mode = scen ? scen[sc].mode : 0;
+    if (mode < 0 || mode > 4) BAD("scenario %d: mode must be in [0, 4]", sc);
     for (int32_t f = 0; f < c->max_funcs; ++f) {
       const ref_func* F = &fn[(int64_t)sc * c->max_funcs + f];
       if (F->kind == K_UNUSED) continue;
@@ -762,6 +779,8 @@ static int32_t validate(const ref_config* c, const ref_scenario* scen, const ref
         BAD("scenario %d func %d: need 1 <= req_pm <= lim_pm <= q_pm", sc, f);
       if (F->req_pm * 32 < om) BAD("scenario %d func %d: req_pm < ceil(omega/32) (Q23)", sc, f);
       if (F->req_pm > om || F->lim_pm > ga) BAD("scenario %d func %d: quota exceeds Omega/gamma", sc, f);
+      if ((mode == 2 || mode == 4) && F->lim_pm > om)
+        BAD("scenario %d func %d: limit above Omega (limit-quota baseline)", sc, f);
       if (F->mem_mib < 1 || F->mem_mib > c->mem_mib) BAD("scenario %d func %d: mem_mib", sc, f);
       if (F->cold_slots < 0) BAD("scenario %d func %d: cold_slots", sc, f);
       if (F->arrive_sec < 0 || F->depart_sec <= F->arrive_sec) BAD("scenario %d func %d: lifecycle", sc, f);
@@ -807,6 +826,15 @@ int32_t dilu_ref_create(const ref_config* cfg, const ref_scenario* scen, const r
     sc->scn_id = scen ? scen[i].scenario_id : i;
     sc->omega_u = scen ? scen[i].omega_pm : cfg->omega_pm;
     sc->gamma_u = scen ? scen[i].gamma_pm : cfg->gamma_pm;
+    sc->mode = scen ? scen[i].mode : M_DILU;
+    /* quota transforms of the baselines: MPS-l and FaST-GS+ run at the
+     * limit quota, MPS-r at the request quota -- both without vertical scaling */
+    for (int32_t f = 0; f < cfg->max_funcs; ++f) {
+      ref_func* F = &s->funcs[(size_t)i * cfg->max_funcs + f];
+      if (F->kind == K_UNUSED) continue;
+      if (sc->mode == M_STATIC_LIMIT || sc->mode == M_EAGER) F->req_pm = F->lim_pm;
+      if (sc->mode == M_STATIC_REQUEST) F->lim_pm = F->req_pm;
+    }
     sc->gpu = (RGpu*)xcalloc((size_t)cfg->gpus_per_scenario, sizeof(RGpu));
     sc->fs = (RFunc*)xcalloc((size_t)cfg->max_funcs, sizeof(RFunc));
     for (int32_t f = 0; f < cfg->max_funcs; ++f)

@@ -43,7 +43,9 @@ typedef struct {
   int32_t n_patterns, pattern_len, flags;           /* flags bit0 LLM split, bit1 invariants */
 } ref_config;
 
-typedef struct { int32_t scenario_id, omega_pm, gamma_pm, reserved; } ref_scenario;
+/* mode: 0 Dilu, 1 Exclusive, 2 StaticLimit (MPS-l), 3 StaticRequest (MPS-r),
+ * 4 EagerHorizontal (FaST-GS+-like) -- baseline modes */
+typedef struct { int32_t scenario_id, omega_pm, gamma_pm, mode; } ref_scenario;
 
 typedef struct {
   int32_t kind, prio, ibs, req_pm, lim_pm, mem_mib, work_per_batch, n_workers;

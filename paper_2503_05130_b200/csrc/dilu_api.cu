@@ -87,6 +87,8 @@ bool check_inputs(const dilu_config* c, const dilu_scenario* scen, const dilu_fu
     const int32_t ga = scen ? scen[s].gamma_pm : c->gamma_pm;
     if (om < 1 || om > c->q_pm) BAD("scenario %d: omega_pm must be in [1, q_pm] (Q12)", s);
     if (ga < om) BAD("scenario %d: gamma_pm < omega_pm", s);
+    const int32_t mode = scen ? scen[s].mode : 0;
+    if (mode < 0 || mode > 4) BAD("scenario %d: mode must be in [0, 4]", s);
     for (int32_t f = 0; f < c->max_funcs; ++f) {
       const dilu_func& F = fn[(size_t)s * c->max_funcs + f];
       if (F.kind == K_UNUSED) continue;
@@ -96,6 +98,8 @@ bool check_inputs(const dilu_config* c, const dilu_scenario* scen, const dilu_fu
         BAD("scenario %d func %d: need 1 <= req_pm <= lim_pm <= q_pm", s, f);
       if ((int64_t)F.req_pm * RES < om) BAD("scenario %d func %d: req_pm < ceil(omega/32) (Q23)", s, f);
       if (F.req_pm > om || F.lim_pm > ga) BAD("scenario %d func %d: quota above Omega/gamma", s, f);
+      if ((mode == 2 || mode == 4) && F.lim_pm > om)
+        BAD("scenario %d func %d: limit above Omega (limit-quota baseline mode)", s, f);
       if (F.mem_mib < 1 || F.mem_mib > c->mem_mib) BAD("scenario %d func %d: mem_mib", s, f);
       if (F.cold_slots < 0) BAD("scenario %d func %d: cold_slots", s, f);
       if (F.arrive_sec < 0 || F.depart_sec <= F.arrive_sec) BAD("scenario %d func %d: lifecycle", s, f);
@@ -290,7 +294,7 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
     hs[i * 4 + 0] = h_scen ? h_scen[i].scenario_id : (int32_t)i;
     hs[i * 4 + 1] = h_scen ? h_scen[i].omega_pm : cfg->omega_pm;
     hs[i * 4 + 2] = h_scen ? h_scen[i].gamma_pm : cfg->gamma_pm;
-    hs[i * 4 + 3] = 0;
+    hs[i * 4 + 3] = h_scen ? h_scen[i].mode : 0;
   }
   rc = cuda_check(s, cudaMemcpyAsync(s->ws + k.scen, hs, S * 16, cudaMemcpyHostToDevice, s->stream),
                   "copy scenarios");

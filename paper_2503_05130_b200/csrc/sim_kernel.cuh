@@ -162,8 +162,9 @@ struct Scn {
   int32_t* flag;             // group-visible broadcast word
   Acc0* z;                   // leader tallies (shared)
   const int32_t* frow;       // this scenario's input function rows [F][16]
-  int32_t scn_id, om, ga;
+  int32_t scn_id, om, ga, mode;   // mode: baseline (0 Dilu, 1 Exclusive, 2 MPS-l, 3 MPS-r, 4 eager)
 };
+enum : int32_t { M_DILU = 0, M_EXCLUSIVE = 1, M_STATIC_LIMIT = 2, M_STATIC_REQUEST = 3, M_EAGER = 4 };
 
 __device__ __forceinline__ int st_of(int32_t meta) { return meta & 3; }
 __device__ __forceinline__ int nst_of(int32_t meta) { return (meta >> 4) & 7; }
@@ -403,6 +404,8 @@ __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
     unsigned long long key;
     if (n == 0) {
       key = (2ull << 62) | (MASK40 << 22) | (unsigned long long)g;  // tier 2, K := 0
+    } else if (c.mode == M_EXCLUSIVE) {
+      continue;                          // pass-through: never share a GPU
     } else {
       const int32_t R = v.gR[g] + req, Lm = v.gL[g] + lim, U = v.gU[g] + mem;
       if (!(R <= c.om && Lm <= c.ga && U <= P.M && n < RES)) continue;
@@ -422,7 +425,7 @@ __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
     c.g.sync();
     return true;
   }
-  if (v.fKind[f] == K_LLM && (P.flags & 1)) {
+  if (v.fKind[f] == K_LLM && (P.flags & 1) && c.mode != M_EXCLUSIVE) {
     // worst-fit split: repeated argmax of free memory over active, cap-feasible GPUs
     int32_t picked[MAXST];
     int32_t pfree[MAXST];
@@ -763,7 +766,7 @@ __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
         kind = fkind[f];
         nst = nst_of(meta);
         req = freq[f] * slot_ms;
-        const int32_t lim = flim[f] * slot_ms;
+        const int32_t lim = c.mode == M_EXCLUSIVE ? T : flim[f] * slot_ms;  // whole GPU
         long long dd;
         if (kind == K_TRAIN) {
           dd = fdtr[f];
@@ -907,8 +910,10 @@ __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, int32_t
         const bool inf = is_inf(kind);
         int32_t* ring = ringb + (size_t)f * W;
         const long long cap1 = fcap1[f];
+        int32_t last = 0;
         if (inf && sec >= 1) {                      // step 1: push second sec-1
           const int32_t val = facc[f];
+          last = val;
           const int32_t head = fhead[f];
           const int32_t ns = fns[f];
           const int32_t thr = fthr[f];
@@ -929,6 +934,16 @@ __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, int32_t
         }
         if (fdep[f] == sec) {                       // step 2: departure
           ev = EV_DEP;
+        } else if (inf && c.mode == M_EAGER) {      // reactive scaling on the last sample
+          if (fns[f] >= 1) {
+            const int32_t n = fnlive[f];
+            if ((long long)last > (long long)n * cap1) {
+              const long long k = ((long long)last + cap1 - 1) / cap1 - n;
+              if (k >= 1) { ev = EV_OUT; v.fK[f] = (int32_t)k; }
+            } else if ((long long)last < (long long)(n - 1) * cap1 && n > P.min_inst) {
+              ev = EV_IN;
+            }
+          }
         } else if (inf && fns[f] >= W) {            // step 3: lazy scaling decision
           const int32_t n = fnlive[f];
           const long long cu = (long long)n * cap1, cd = (long long)(n - 1) * cap1;
@@ -1050,6 +1065,7 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
   c.scn_id = P.scen[sc * 4 + 0];
   c.om = P.scen[sc * 4 + 1];
   c.ga = P.scen[sc * 4 + 2];
+  c.mode = P.scen[sc * 4 + 3];
   Acc acc = {};
   acc.z = &red.z;
   c.z = &red.z;
@@ -1256,17 +1272,21 @@ __global__ void k_init(Params P) {
     v.iR[s] = 0; v.iR[P.I + s] = 0; v.iBmin[s] = BIG; v.iBmin[P.I + s] = BIG;
     v.fstack[s] = P.I - 1 - s;
   }
+  const int32_t mode = P.scen[sc * 4 + 3];
   for (int32_t f = threadIdx.x; f < P.F; f += blockDim.x) {
     const int32_t* r = rows + (size_t)f * 16;
     const int32_t kind = r[0];
-    v.fKind[f] = kind; v.fPrio[f] = r[1]; v.fIbs[f] = r[2] > 0 ? r[2] : 1; v.fReq[f] = r[3];
-    v.fLim[f] = r[4]; v.fMem[f] = r[5]; v.fCb[f] = r[6] > 0 ? r[6] : 1; v.fNw[f] = r[7];
+    // baseline quota transforms: limit-quota modes run at lim, MPS-r at req
+    const int32_t req = (mode == M_STATIC_LIMIT || mode == M_EAGER) ? r[4] : r[3];
+    const int32_t limq = mode == M_STATIC_REQUEST ? r[3] : r[4];
+    v.fKind[f] = kind; v.fPrio[f] = r[1]; v.fIbs[f] = r[2] > 0 ? r[2] : 1; v.fReq[f] = req;
+    v.fLim[f] = limq; v.fMem[f] = r[5]; v.fCb[f] = r[6] > 0 ? r[6] : 1; v.fNw[f] = r[7];
     v.fCold[f] = r[9]; v.fCls[f] = r[10]; v.fPat[f] = r[13]; v.fScale[f] = r[14];
     v.fPhase[f] = r[15];
-    const long long lim_tok = (long long)r[4] * P.slot_ms;
+    const long long lim_tok = (long long)limq * P.slot_ms;
     v.fDtr[f] = kind == K_TRAIN ? (int32_t)(lim_tok * r[8] / 1000) : 0;
     // R5: cap1 = (1000/slot_ms) * floor(req_tok / c_b) * IBS
-    v.fCap1[f] = is_inf(kind) ? (long long)P.SPS * (((long long)r[3] * P.slot_ms) / r[6]) * r[2] : 0;
+    v.fCap1[f] = is_inf(kind) ? (long long)P.SPS * (((long long)req * P.slot_ms) / r[6]) * r[2] : 0;
     v.fReg[f] = 0; v.fNsamp[f] = 0; v.fAcc[f] = 0; v.fHead[f] = 0; v.fUp[f] = 0; v.fDown[f] = 0;
     v.fThrn[f] = -1; v.fNlive[f] = 0; v.fLh[f] = -1; v.fLt[f] = -1;
     v.fGang[f] = BIG; v.fGang[P.F + f] = BIG; v.fFlag[f] = 0; v.fK[f] = 0; v.fList[f] = 0;

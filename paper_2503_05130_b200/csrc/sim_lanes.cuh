@@ -144,7 +144,7 @@ struct Ctx {
   const LV* vp;         // shared
   const LParams* P;
   const int32_t* frow;  // this scenario's input rows
-  int32_t scn_id, om, ga, k, lane;
+  int32_t scn_id, om, ga, mode, k, lane;
   bool active;
 };
 
@@ -450,6 +450,8 @@ struct Engine {
       unsigned long long key;
       if (n == 0) {
         key = (2ull << 62) | (MASK40 << 22) | (unsigned long long)g;
+      } else if (c.mode == M_EXCLUSIVE) {
+        continue;
       } else {
         const int32_t R = AT(v.gR, g) + req, Lm = AT(v.gL, g) + lim, U = AT(v.gU, g) + mem;
         if (!(R <= c.om && Lm <= c.ga && U <= Pm.M && n < RES)) continue;
@@ -538,7 +540,7 @@ struct Engine {
           if (tier <= 1) {
             l_commit(c, s, (int32_t)(best & 0x3FFFFF), AT(v.fMem, f));
             sh.mode[L] = 3;  // member placed
-          } else if (AT(v.fKind, f) == K_LLM && (Pm.flags & 1)) {
+          } else if (AT(v.fKind, f) == K_LLM && (Pm.flags & 1) && c.mode != M_EXCLUSIVE) {
             sh.mode[L] = 2;  // worst-fit split rounds
             sh.nsplit[L] = 0;
             sh.sdone[L] = 0;
@@ -654,8 +656,10 @@ struct Engine {
             const bool inf = inf_l(kind);
             int32_t* ring = v.ring + ((size_t)f * W << 5);
             const long long cap1 = AT(v.fCap1, f);
+            int32_t last = 0;
             if (inf && sec >= 1) {                    // step 1: push second sec-1
               const int32_t val = AT(v.fAcc, f);
+              last = val;
               const int32_t head = AT(v.fHead, f);
               const int32_t ns = AT(v.fNsamp, f);
               const int32_t thr = AT(v.fThrn, f);
@@ -673,6 +677,16 @@ struct Engine {
             }
             if (AT(v.fDep, f) == sec) {               // step 2: departure
               ev = EV_DEP;
+            } else if (inf && c.mode == M_EAGER) {
+              if (AT(v.fNsamp, f) >= 1) {
+                const int32_t n = AT(v.fNlive, f);
+                if ((long long)last > (long long)n * cap1) {
+                  const long long kk = ((long long)last + cap1 - 1) / cap1 - n;
+                  if (kk >= 1) { ev = EV_OUT; AT(v.fK, f) = (int32_t)kk; }
+                } else if ((long long)last < (long long)(n - 1) * cap1 && n > Pm.min_inst) {
+                  ev = EV_IN;
+                }
+              }
             } else if (inf && AT(v.fNsamp, f) >= W) { // step 3: lazy scaling decision
               const int32_t n = AT(v.fNlive, f);
               const long long cu = (long long)n * cap1, cd = (long long)(n - 1) * cap1;
@@ -822,7 +836,7 @@ struct Engine {
         if (AT(v.rReady, e) > t) continue;                 // cold: a = e = 0 (Q14)
         const int32_t info = AT(v.rInfo, e);
         const int32_t kind = info & 15, nst = (info >> 4) & 7;
-        const int32_t req = AT(v.rReq, e), lim = AT(v.rLim, e);
+        const int32_t req = AT(v.rReq, e), lim = c.mode == M_EXCLUSIVE ? T : AT(v.rLim, e);
         int32_t d, need = 0, rr = 0, cst = 1, ibs = 1;
         if (kind == K_TRAIN) {
           d = AT(v.rDtr, e);
@@ -943,6 +957,7 @@ __global__ void __launch_bounds__(32 * P) k_lanes(LParams Pin, int32_t* next_grp
     c.scn_id = c.active ? Pm.scen[scn * 4 + 0] : 0;
     c.om = c.active ? Pm.scen[scn * 4 + 1] : 0;
     c.ga = c.active ? Pm.scen[scn * 4 + 2] : 0;
+    c.mode = c.active ? Pm.scen[scn * 4 + 3] : 0;
     const LV& v = *c.vp;
     const int LANE = c.lane;
     if (c.active && AT(v.h, LH_ERR)) c.active = false;
@@ -1057,17 +1072,20 @@ __global__ void k_lanes_init(LParams P) {
   for (int k = 0; k < RLOG; ++k) { AT(v.rlG, k) = 0; AT(v.rlE, k) = 0; }
   const bool active = scn < P.S;
   const int32_t* rows = P.funcs + (size_t)(active ? scn : 0) * P.F * 16;
+  const int32_t mode = active ? P.scen[scn * 4 + 3] : 0;
   for (int32_t f = 0; f < P.F; ++f) {
     const int32_t* r = rows + (size_t)f * 16;
     const int32_t kind = active ? r[0] : K_UNUSED;
+    const int32_t req = (mode == M_STATIC_LIMIT || mode == M_EAGER) ? r[4] : r[3];
+    const int32_t limq = mode == M_STATIC_REQUEST ? r[3] : r[4];
     AT(v.fKind, f) = kind; AT(v.fPrio, f) = r[1]; AT(v.fIbs, f) = r[2] > 0 ? r[2] : 1;
-    AT(v.fReq, f) = r[3]; AT(v.fLim, f) = r[4]; AT(v.fMem, f) = r[5];
+    AT(v.fReq, f) = req; AT(v.fLim, f) = limq; AT(v.fMem, f) = r[5];
     AT(v.fCb, f) = r[6] > 0 ? r[6] : 1; AT(v.fNw, f) = r[7]; AT(v.fCold, f) = r[9];
     AT(v.fCls, f) = r[10]; AT(v.fArr, f) = r[11]; AT(v.fDep, f) = r[12]; AT(v.fPat, f) = r[13];
     AT(v.fScale, f) = r[14];
-    const long long lim_tok = (long long)r[4] * P.slot_ms;
+    const long long lim_tok = (long long)limq * P.slot_ms;
     AT(v.fDtr, f) = kind == K_TRAIN ? (int32_t)(lim_tok * r[8] / 1000) : 0;
-    AT(v.fCap1, f) = inf_l(kind) ? (long long)P.SPS * (((long long)r[3] * P.slot_ms) / (r[6] > 0 ? r[6] : 1)) * r[2] : 0;
+    AT(v.fCap1, f) = inf_l(kind) ? (long long)P.SPS * (((long long)req * P.slot_ms) / (r[6] > 0 ? r[6] : 1)) * r[2] : 0;
     AT(v.fReg, f) = 0; AT(v.fNsamp, f) = 0; AT(v.fAcc, f) = 0; AT(v.fHead, f) = 0;
     AT(v.fUp, f) = 0; AT(v.fDown, f) = 0; AT(v.fThrn, f) = -1; AT(v.fNlive, f) = 0;
     AT(v.fLh, f) = -1; AT(v.fLt, f) = -1; AT(v.fGang, f) = BIG; AT(v.fGang, P.F + f) = BIG;

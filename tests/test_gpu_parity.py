@@ -218,3 +218,20 @@ def test_c3_full_day():
     """C3 (1,024 GPUs, 24 h at 1 s slots): every tally of the whole day."""
     wl = di.c3(T=86400)
     run_pair(wl, [86400], snap=False)
+
+
+# ------------------------------------------------------ baseline modes (s8(f) #1)
+
+@pytest.mark.parametrize("mode", [1, 2, 3, 4])
+def test_baseline_mode_c2(mode):
+    wl = di.with_modes(di.c2(seed=6, T=900), [mode])
+    run_pair(wl, [1, 299, 600], id_cap=4096)
+
+
+@pytest.mark.parametrize("engine", ["cta", "lanes", "cluster"])
+def test_mixed_modes_c4_slice(engine, monkeypatch):
+    """40 C4 sweep points, scenario i under mode i % 5, every engine."""
+    monkeypatch.setenv("DILU_ENGINE", engine)
+    wl = di.c4(n_scenarios=4096, T=600).subset(np.arange(3, 4096, 102))
+    wl = di.with_modes(wl, np.arange(wl.S) % 5)
+    run_pair(wl, [1, 599], id_cap=2048)
