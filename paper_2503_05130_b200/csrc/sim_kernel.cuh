@@ -238,6 +238,7 @@ __device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
   View& v = c.v;
   const int32_t f = v.iFunc[s];
   if (v.gN[g] == 0) v.h[H_NACT] += 1;
+  v.gMask[g] |= 1ull << (v.fCls[f] & 63);
   v.gR[g] += v.fReq[f];
   v.gL[g] += v.fLim[f];
   v.gU[g] += share;
@@ -277,6 +278,9 @@ __device__ void release(Scn& c, int32_t s) {
     for (; j + 1 < nr; ++j) res[j] = res[j + 1];
     v.gN[g] = nr - 1;
     if (nr - 1 == 0) v.h[H_NACT] -= 1;
+    unsigned long long m = 0;
+    for (int x = 0; x < nr - 1; ++x) m |= 1ull << (v.fCls[v.iFunc[res[x]]] & 63);
+    v.gMask[g] = m;
     v.iG[s * MAXST + k] = -1;
   }
   v.iMeta[s] = meta & ~(7 << 4);
@@ -410,8 +414,10 @@ __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
       const int32_t R = v.gR[g] + req, Lm = v.gL[g] + lim, U = v.gU[g] + mem;
       if (!(R <= c.om && Lm <= c.ga && U <= P.M && n < RES)) continue;
       const int32_t* res = v.gRes + (size_t)g * RES;
+      // affinity: the class bitmask rules most GPUs out exactly; scan on a hit
       int aff = 0;
-      for (int j = 0; j < n && !aff; ++j) aff = (v.fCls[v.iFunc[res[j]]] == cls);
+      if ((v.gMask[g] >> (cls & 63)) & 1ull)
+        for (int j = 0; j < n && !aff; ++j) aff = (v.fCls[v.iFunc[res[j]]] == cls);
       const unsigned long long K = (unsigned long long)(aM * R + bQ * U);
       key = ((unsigned long long)(aff ? 0 : 1) << 62) | ((MASK40 - K) << 22) |
             (unsigned long long)g;
@@ -1263,6 +1269,7 @@ __global__ void k_init(Params P) {
   for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
     v.gR[g] = 0; v.gL[g] = 0; v.gU[g] = 0; v.gN[g] = 0; v.gExcl[g] = 0; v.gGrow[g] = 0;
     v.gRel[g] = 0;
+    v.gMask[g] = 0;
   }
   for (int32_t k = threadIdx.x; k < P.G * RES; k += blockDim.x) v.gRes[k] = -1;
   for (int32_t s = threadIdx.x; s < P.I; s += blockDim.x) {
