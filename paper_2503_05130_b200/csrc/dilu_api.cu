@@ -135,6 +135,18 @@ int choose_engine(const dilu_config* c) {
   }
   return e;
 }
+// Fused-batch length: with sub-second slots the SPS slots between two
+// second boundaries share one placement state, so P0/P1/P2 run once per batch of up to
+// 16 slots.  DILU_BATCH=n (1..16) is a tuning/test hook; 1 runs every slot separately.
+int choose_batch(const dilu_config* c) {
+  const int sps = 1000 / c->slot_ms;
+  int b = sps < 16 ? sps : 16;
+  if (const char* v = getenv("DILU_BATCH")) {
+    const int x = atoi(v);
+    if (x >= 1 && x <= 16) b = x < sps ? x : sps;
+  }
+  return b < 1 ? 1 : b;
+}
 int choose_parts() {
   int p = 8;
   if (const char* v = getenv("DILU_PARTS")) {
@@ -244,7 +256,7 @@ size_t dilu_workspace_bytes(const dilu_config* cfg) {
   char msg[256];
   if (!check_cfg(cfg, msg, sizeof msg)) return 0;
   const Layout L = make_layout(cfg->gpus_per_scenario, cfg->max_funcs, cfg->max_instances,
-                               cfg->window_s);
+                               cfg->window_s, choose_batch(cfg));
   return carve(cfg, L).total;
 }
 
@@ -263,7 +275,8 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   if (!s) return DILU_E_USAGE;
   s->cfg = *cfg;
   s->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
-  s->L = make_layout(cfg->gpus_per_scenario, cfg->max_funcs, cfg->max_instances, cfg->window_s);
+  s->L = make_layout(cfg->gpus_per_scenario, cfg->max_funcs, cfg->max_instances, cfg->window_s,
+                     choose_batch(cfg));
   const Carve k = carve(cfg, s->L);
   if (!d_workspace || ws_bytes < k.total || (reinterpret_cast<uintptr_t>(d_workspace) % ALIGN)) {
     fprintf(stderr, "dilu_sim_create: workspace needs %zu bytes, 256-byte aligned (got %zu)\n",

@@ -880,6 +880,229 @@ __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
   }
 }
 
+// ---- fused batches (sub-second slots) ---------------------------------------------------
+// Between two second boundaries nothing mutates the placement (scaling and
+// placement run at t mod SPS == 0 only), so the slots t..t+B-1 of one batch see the same
+// residents, rows and functions; only the arrivals A_f(u) and the warm set (ready <= u)
+// change.  P0b/P1b/P2b load each function / resident once and loop over the batch's slots,
+// writing the per-slot r, stage minimum and gang into the [B][I] / [B][F] buffers.  The
+// arithmetic per slot is exactly that of phase0/1/2 (same expressions, same order of the
+// integer operations), so results are bit-identical; only the hash summation order moves
+// (it is a mod-2^64 sum, order-free by construction, R8).
+
+__device__ void phase0_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
+  View& v = c.v;
+  const Params& P = *c.P;
+  const int32_t* __restrict__ infl = v.fInfL;
+  const int32_t* __restrict__ reg = v.fReg;
+  int32_t* __restrict__ pidx = v.fPidx;
+  const int32_t* __restrict__ lh = v.fLh;
+  const int32_t* __restrict__ nxt = v.iNext;
+  const int32_t* __restrict__ meta = v.iMeta;
+  const int32_t* __restrict__ ready = v.iReady;
+  int32_t* __restrict__ rb = v.rB;
+  const int32_t Tp = P.Tp, ninf = v.h[H_NINF], I = P.I;
+  for (int32_t k = c.g.rank(); k < ninf; k += c.g.size()) {
+    const int32_t f = infl[k];
+    if (!reg[f]) continue;
+    const int32_t* __restrict__ prow = P.pat + (size_t)v.fPat[f] * Tp;
+    const long long scale = v.fScale[f];
+    const int32_t s0 = lh[f];
+    int32_t idx = pidx[f];
+    // warm set over the batch: instances placed and ready by t, plus those turning warm
+    // inside it (cold starts finishing mid-batch)
+    int32_t nw0 = 0, rmin = BIG;
+    for (int32_t s = s0; s >= 0; s = nxt[s]) {
+      if (st_of(meta[s]) != ST_PLACED) continue;
+      const int32_t rd = ready[s];
+      if (rd <= t) ++nw0; else rmin = rd < rmin ? rd : rmin;
+    }
+    int32_t asum = 0;
+    for (int32_t u = 0; u < B; ++u) {
+      const int32_t tu = t + u;
+      const long long x = __ldg(prow + idx);
+      idx = idx + 1 == Tp ? 0 : idx + 1;
+      const int32_t A = (int32_t)((x * scale) >> 10);
+      acc.nfun += 1;
+      asum += A;
+      acc.rtot += A;
+      int32_t nw = nw0;
+      if (rmin <= tu) {
+        nw = 0;
+        for (int32_t s = s0; s >= 0; s = nxt[s]) nw += (st_of(meta[s]) == ST_PLACED && ready[s] <= tu);
+      }
+      if (nw == 0) { acc.rvio += A; continue; }
+      const int32_t q = A / nw, rem = A - q * nw;
+      int32_t rank = 0;
+      int32_t* __restrict__ ru = rb + (size_t)u * I;
+      for (int32_t s = s0; s >= 0; s = nxt[s]) {
+        if (st_of(meta[s]) == ST_PLACED && ready[s] <= tu) {
+          ru[s] = q + (rank < rem ? 1 : 0);
+          ++rank;
+        }
+      }
+    }
+    pidx[f] = idx;
+    v.fAcc[f] += asum;
+  }
+}
+
+__device__ void phase1_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
+  View& v = c.v;
+  const Params& P = *c.P;
+  const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
+  const int32_t* __restrict__ cbase = v.h + H_CBASE;
+  const int32_t* __restrict__ ccnt = v.h + H_CCNT;
+  const int32_t* __restrict__ gbase = v.h + H_GBASE;
+  const int32_t nch = cbase[6];
+  const int32_t T = (int32_t)P.T_slot, slot_ms = P.slot_ms, I = P.I, F = P.F;
+  const uint64_t hs = sm64((uint32_t)c.scn_id);
+  for (int32_t ch = wid; ch < nch; ch += nwarp) {
+    int k = 0;
+#pragma unroll
+    for (int x = 1; x < 6; ++x) k += (ch >= cbase[x]);
+    const int w = 1 << k;
+    const int32_t gi = (ch - cbase[k]) * (32 >> k) + (lane >> k);
+    int32_t g = -1, s = -1;
+    if (gi < ccnt[k]) {
+      g = v.gGrow[gbase[k] + gi];
+      const int j = lane & (w - 1);
+      if (j < v.gN[g]) s = v.gRes[(size_t)g * RES + j];
+    }
+    // batch-invariant resident fields
+    bool placed = false;
+    int32_t rd = BIG, f = -1, kind = 0, nst = 1, cst = 1, ibs = 1, req0 = 0, lim = 0, id = 0;
+    long long dtr = 0;
+    if (s >= 0) {
+      const int32_t meta = v.iMeta[s];
+      placed = st_of(meta) == ST_PLACED;
+      if (placed) {
+        rd = v.iReady[s];
+        f = v.iFunc[s];
+        id = v.iId[s];
+        kind = v.fKind[f];
+        nst = nst_of(meta);
+        req0 = v.fReq[f] * slot_ms;
+        lim = c.mode == M_EXCLUSIVE ? T : v.fLim[f] * slot_ms;
+        if (kind == K_TRAIN) {
+          dtr = v.fDtr[f];
+        } else {
+          ibs = v.fIbs[f];
+          const int32_t cb = v.fCb[f];
+          cst = nst == 1 ? cb : (cb + nst - 1) / nst;
+        }
+      }
+    }
+    const uint64_t gk = uint64_t((uint32_t)g) << 32;
+    for (int32_t u = 0; u < B; ++u) {
+      const int32_t tu = t + u;
+      const bool warm = placed && rd <= tu;
+      int32_t req = 0, want = 0, rr = 0, need = 0, d = 0;
+      if (warm) {
+        req = req0;
+        long long dd;
+        if (kind == K_TRAIN) {
+          dd = dtr;
+        } else {
+          rr = v.rB[(size_t)u * I + s];
+          need = rr / ibs + (rr % ibs != 0);
+          dd = (long long)need * cst;
+        }
+        d = dd < lim ? (int32_t)dd : lim;
+        want = d > req ? d - req : 0;
+        if (kind == K_TRAIN) d = (int32_t)dd;
+      }
+      int32_t incl = want, sreq = req;
+      for (int o = 1; o < w; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o, w);
+        if ((lane & (w - 1)) >= o) incl += y;
+      }
+      for (int o = w >> 1; o > 0; o >>= 1) sreq += __shfl_xor_sync(0xffffffffu, sreq, o, w);
+      if (warm) {
+        const int32_t room = T - sreq - (incl - want);
+        const int32_t sp = want < room ? want : (room > 0 ? room : 0);
+        const int32_t a = req + sp;
+        acc.nres += 1;
+        const uint64_t ht = sm64(hs ^ (uint32_t)tu);
+        acc.hash += sm64(sm64(ht ^ (uint32_t)id) ^ (gk | (uint32_t)a));
+        if (kind == K_TRAIN) {
+          atomicMin(&v.gB[(size_t)u * F + f], d < a ? d : a);
+        } else {
+          const int32_t fit = a / cst;
+          const int32_t b = need < fit ? need : fit;
+          if (nst == 1) {
+            const long long cap = (long long)b * ibs;
+            const int32_t served = cap < rr ? (int32_t)cap : rr;
+            acc.rsrv += served;
+            acc.rvio += rr - served;
+            const long long e = (long long)b * cst;
+            acc.iexe += e;
+            acc.etot += e;
+          } else {
+            atomicMin(&v.bB[(size_t)u * I + s], b);
+          }
+        }
+      }
+    }
+  }
+}
+
+__device__ void phase2_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
+  View& v = c.v;
+  const Params& P = *c.P;
+  const int32_t* __restrict__ defl = v.fDefL;
+  const int32_t* __restrict__ lh = v.fLh;
+  const int32_t* __restrict__ nxt = v.iNext;
+  const int32_t* __restrict__ meta = v.iMeta;
+  const int32_t ndef = v.h[H_NDEF], I = P.I, F = P.F;
+  for (int32_t k = c.g.rank(); k < ndef; k += c.g.size()) {
+    const int32_t f = defl[k];
+    if (!v.fReg[f]) continue;
+    if (v.fKind[f] == K_TRAIN) {
+      int32_t nlive = 0, rmax = 0;
+      bool placed = true;
+      for (int32_t s = lh[f]; s >= 0; s = nxt[s]) {
+        ++nlive;
+        placed &= st_of(meta[s]) == ST_PLACED;
+        const int32_t rd = v.iReady[s];
+        rmax = rd > rmax ? rd : rmax;
+      }
+      const long long nwk = v.fNw[f];
+      for (int32_t u = 0; u < B; ++u) {
+        int32_t* gp = &v.gB[(size_t)u * F + f];
+        const int32_t gm = *gp;
+        if (gm == BIG) continue;
+        *gp = BIG;
+        if (placed && rmax <= t + u) {
+          acc.tprg += nwk * gm;
+          acc.etot += (long long)nlive * gm;
+        }
+      }
+    } else {
+      const int32_t ibs = v.fIbs[f], cb = v.fCb[f];
+      for (int32_t s = lh[f]; s >= 0; s = nxt[s]) {
+        const int32_t nst = nst_of(meta[s]);
+        if (nst <= 1) continue;
+        const int32_t cst = (cb + nst - 1) / nst;
+        for (int32_t u = 0; u < B; ++u) {
+          int32_t* bp = &v.bB[(size_t)u * I + s];
+          const int32_t b = *bp;
+          if (b == BIG) continue;
+          *bp = BIG;
+          const int32_t rr = v.rB[(size_t)u * I + s];
+          const long long cap = (long long)b * ibs;
+          const int32_t served = cap < rr ? (int32_t)cap : rr;
+          acc.rsrv += served;
+          acc.rvio += rr - served;
+          const long long e = (long long)nst * b * cst;
+          acc.iexe += e;
+          acc.etot += e;
+        }
+      }
+    }
+  }
+}
+
 // ---- boundary -----------------------------------------------------------------------
 
 enum : int32_t { EV_DEP = 1, EV_OUT = 2, EV_IN = 4, EV_ARR = 8 };
@@ -1105,6 +1328,7 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
   } else {
     // ---- dilu_scale_step: the slot loop
     for (int32_t t = t0; t < t0 + n_slots; ++t) {
+      const bool fused = P.L.B > 1;
 #ifdef DILU_PHASE_TIMING
       long long tk0 = clock64(), tk1;
 #define TICK(slot) do { tk1 = clock64(); if (c.g.leader()) acc.z->st[8 + (slot)] += tk1 - tk0; tk0 = tk1; } while (0)
@@ -1119,7 +1343,7 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
         const int32_t f0 = c.g.rank() * per;
         if (f0 < P.F && v.fReg[f0]) pf_ring = v.ring[(size_t)f0 * P.W + v.fHead[f0]];
       }
-      {
+      if (!fused) {
         const int32_t k = c.g.rank();
         if (k < v.h[H_NINF]) {
           const int32_t f = v.fInfL[k];
@@ -1139,6 +1363,31 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
         if (c.g.leader()) acc.z->st[S_LAYOUT] += 1;
       }
       TICK(2);
+      if (fused) {
+        // one fused batch: the slots up to the next second boundary (<= L.B of them)
+        int32_t B = P.SPS - t % P.SPS;
+        if (B > t0 + n_slots - t) B = t0 + n_slots - t;
+        if (B > P.L.B) B = P.L.B;
+        if (t % P.SPS != 0) c.g.sync();   // previous batch's P2 has read rB / bB
+        phase0_b(c, t, B, acc);
+        if (c.g.leader()) {
+          const long long na = v.h[H_NACT];
+          acc.z->act += na * B;
+          acc.z->memu += (na * P.M - v.h[H_SUMU]) * B;
+          acc.z->rows += (long long)P.G * B;
+          acc.z->maxa = na > acc.z->maxa ? na : acc.z->maxa;
+          acc.z->st[S_SLOT] += B;
+        }
+        c.g.sync();
+        TICK(3);
+        phase1_b(c, t, B, acc);
+        c.g.sync();
+        TICK(4);
+        phase2_b(c, t, B, acc);
+        TICK(5);
+        t += B - 1;
+        continue;
+      }
       phase0(c, t, acc, pf_f, pf_x);
       if (c.g.leader()) {
         const long long na = v.h[H_NACT];
@@ -1290,7 +1539,8 @@ __global__ void k_init(Params P) {
     v.fLim[f] = limq; v.fMem[f] = r[5]; v.fCb[f] = r[6] > 0 ? r[6] : 1; v.fNw[f] = r[7];
     v.fCold[f] = r[9]; v.fCls[f] = r[10]; v.fPat[f] = r[13]; v.fScale[f] = r[14];
     v.fPhase[f] = r[15];
-    const long long lim_tok = (long long)limq * P.slot_ms;
+    // training demand d = lim * duty; Exclusive owns the whole GPU (lim = T_slot, D7)
+    const long long lim_tok = (long long)(mode == M_EXCLUSIVE ? 1000 : limq) * P.slot_ms;
     v.fDtr[f] = kind == K_TRAIN ? (int32_t)(lim_tok * r[8] / 1000) : 0;
     // R5: cap1 = (1000/slot_ms) * floor(req_tok / c_b) * IBS
     v.fCap1[f] = is_inf(kind) ? (long long)P.SPS * (((long long)req * P.slot_ms) / r[6]) * r[2] : 0;
@@ -1298,6 +1548,10 @@ __global__ void k_init(Params P) {
     v.fThrn[f] = -1; v.fNlive[f] = 0; v.fLh[f] = -1; v.fLt[f] = -1;
     v.fGang[f] = BIG; v.fGang[P.F + f] = BIG; v.fFlag[f] = 0; v.fK[f] = 0; v.fList[f] = 0;
     v.fArr[f] = r[11]; v.fDep[f] = r[12]; v.fPidx[f] = 0;
+  }
+  if (P.L.B > 1) {
+    for (size_t k = threadIdx.x; k < (size_t)P.L.B * P.I; k += blockDim.x) v.bB[k] = BIG;
+    for (size_t k = threadIdx.x; k < (size_t)P.L.B * P.F; k += blockDim.x) v.gB[k] = BIG;
   }
   if (threadIdx.x == 0) {   // static lists: inference functions (P0), training + LLM (P2)
     int32_t ni = 0, nd = 0;

@@ -1083,7 +1083,8 @@ __global__ void k_lanes_init(LParams P) {
     AT(v.fCb, f) = r[6] > 0 ? r[6] : 1; AT(v.fNw, f) = r[7]; AT(v.fCold, f) = r[9];
     AT(v.fCls, f) = r[10]; AT(v.fArr, f) = r[11]; AT(v.fDep, f) = r[12]; AT(v.fPat, f) = r[13];
     AT(v.fScale, f) = r[14];
-    const long long lim_tok = (long long)limq * P.slot_ms;
+    // training demand d = lim * duty; Exclusive owns the whole GPU (lim = T_slot, D7)
+    const long long lim_tok = (long long)(mode == M_EXCLUSIVE ? 1000 : limq) * P.slot_ms;
     AT(v.fDtr, f) = kind == K_TRAIN ? (int32_t)(lim_tok * r[8] / 1000) : 0;
     AT(v.fCap1, f) = inf_l(kind) ? (long long)P.SPS * (((long long)req * P.slot_ms) / (r[6] > 0 ? r[6] : 1)) * r[2] : 0;
     AT(v.fReg, f) = 0; AT(v.fNsamp, f) = 0; AT(v.fAcc, f) = 0; AT(v.fHead, f) = 0;

@@ -38,7 +38,7 @@ enum : int {
 };
 
 struct Layout {
-  int32_t G, F, I, W;
+  int32_t G, F, I, W, B;   // B: slots per fused batch between second boundaries (1 = unfused)
   // byte offsets inside one block
   size_t hdr;
   size_t gR, gL, gU, gN, gRes, gExcl, gGrow, gMask, gRel, rlG, rlE;
@@ -48,14 +48,15 @@ struct Layout {
   size_t fReg, fNsamp, fAcc, fHead, fUp, fDown, fThrn, fNlive, fLh, fLt, fGang, fFlag, fK,
       fList, fArr, fDep, fPidx, fInfL, fDefL;
   size_t qFunc, qFirst, qN, qFail, qSlot, iQ;
+  size_t rB, bB, gB;       // per-batch-slot r, LLM stage minimum, training gang (B > 1 only)
   size_t hot_bytes, bytes;
 };
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W) {
+inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B = 1) {
   Layout L;
-  L.G = G; L.F = F; L.I = I; L.W = W;
+  L.G = G; L.F = F; L.I = I; L.W = W; L.B = B;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t at = o; o = align16(o + bytes); return at; };
   // hot region: touched every slot -> staged in shared memory when it fits
@@ -90,6 +91,10 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W) {
   L.iSh0 = take(4 * (size_t)I);         // stage-0 memory share
   L.iShare = take(4 * (size_t)I * MAXST);
   L.iBmin = take(4 * 2 * (size_t)I);
+  // fused-batch buffers [B][I] / [B][F] (slot-major): the slots between two second
+  // boundaries share one placement state, so P0/P1/P2 run once per batch
+  const size_t bb = B > 1 ? (size_t)B : 0;
+  L.rB = take(4 * bb * I); L.bB = take(4 * bb * I); L.gB = take(4 * bb * F);
   L.bytes = align16(o);
   return L;
 }
@@ -107,6 +112,7 @@ struct View {
   int32_t *fReg, *fNsamp, *fAcc, *fHead, *fUp, *fDown, *fThrn, *fNlive, *fLh, *fLt, *fGang,
       *fFlag, *fK, *fList, *fArr, *fDep, *fPidx, *fInfL, *fDefL;
   int32_t *qFunc, *qFirst, *qN, *qFail, *qSlot, *iQ;
+  int32_t *rB, *bB, *gB;
   int32_t* ring;  // global [F][W]
 };
 
@@ -130,6 +136,7 @@ inline View make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
   P32(fLh); P32(fLt); P32(fGang); P32(fFlag); P32(fK); P32(fList); P32(fArr); P32(fDep);
   P32(fPidx); P32(fInfL); P32(fDefL);
   P32(qFunc); P32(qFirst); P32(qN); P32(qFail); P32(qSlot); P32(iQ);
+  P32(rB); P32(bB); P32(gB);
 #undef P32
   v.ring = nullptr;
   return v;

@@ -235,3 +235,23 @@ def test_mixed_modes_c4_slice(engine, monkeypatch):
     wl = di.c4(n_scenarios=4096, T=600).subset(np.arange(3, 4096, 102))
     wl = di.with_modes(wl, np.arange(wl.S) % 5)
     run_pair(wl, [1, 599], id_cap=2048)
+
+
+# ------------------------------------------- fused sub-second batches
+
+@pytest.mark.parametrize("shape", ["cluster_b10", "cluster_b3", "cluster_b1", "cta_b10",
+                                   "cta_b4"])
+def test_fused_batches(shape, monkeypatch):
+    """100 ms slots: the slots between two second boundaries run as one fused batch
+    (DILU_BATCH = batch cap).  Cold starts shifted by 3 slots end mid-batch, calls start
+    and end mid-window, and the five scenarios run modes 0..4."""
+    engine, _, b = shape.partition("_")
+    monkeypatch.setenv("DILU_ENGINE", engine)
+    monkeypatch.setenv("DILU_BATCH", b[1:])
+    wl = di.scaled("C5b", 512, 60, 120, 360, 100, 600, [53, 54, 55, 56, 57], max_instances=8192)
+    funcs = wl.funcs.copy()
+    live = funcs[:, :, di.FI["kind"]] >= 0
+    funcs[:, :, di.FI["cold_slots"]] += 3 * live
+    wl = di.with_modes(di.Workload("C5b", wl.cfg, wl.scen, funcs, wl.patterns, wl.n_slots),
+                       [0, 1, 2, 3, 4])
+    run_pair(wl, [1, 13, 7, 279, 300], id_cap=16384)

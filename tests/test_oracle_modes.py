@@ -93,3 +93,13 @@ def test_eager_scales_on_first_sample_lazy_absorbs():
     assert dilu[T["scale_out_events"]] == 0 and dilu[T["cold_starts"]] == 1
     assert eager[T["scale_out_events"]] >= 1 and eager[T["scale_in_events"]] >= 1
     assert eager[T["cold_starts"]] > dilu[T["cold_starts"]]
+
+
+def test_exclusive_training_runs_at_duty_of_whole_gpu():
+    """Exclusive pass-through (D7): a lone worker with duty 0.8 owns the GPU, so
+    its demand and grant are 0.8 * T_slot per slot (P:351 comm idle), not 0.8 * limit."""
+    wl = tiny([dict(kind=2, prio=1, n_workers=1, req_pm=300, lim_pm=600, mem_mib=4096,
+                    duty_pm=800, arrive_sec=0, depart_sec=IDLE[1], cold_slots=0)], G=2,
+              T_pat=20)
+    assert run_mode(wl, 1, 20)[T["train_progress_tokens"]] == 20 * 800_000
+    assert run_mode(wl, 0, 20)[T["train_progress_tokens"]] == 20 * 480_000
