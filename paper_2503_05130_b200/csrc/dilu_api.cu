@@ -230,7 +230,7 @@ dilu_status launch_run(dilu_sim* s, int32_t n_slots, int32_t n_req, const int32_
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    rc = cuda_check(s, cudaLaunchKernelEx(&lc, k_run_cluster, s->P, s->t, n_slots, n_req, rs, rf, og, oi),
+    rc = cuda_check(s, cudaLaunchKernelEx(&lc, s->L.B > 1 ? k_run_cluster<true> : k_run_cluster<false>, s->P, s->t, n_slots, n_req, rs, rf, og, oi),
                     "k_run_cluster launch");
     if (rc) return rc;
     return cuda_check(s, cudaGetLastError(), "k_run_cluster");
@@ -241,10 +241,11 @@ dilu_status launch_run(dilu_sim* s, int32_t n_slots, int32_t n_req, const int32_
       case 16: lanes::k_lanes<16><<<grid, block, 0, s->stream>>>(s->LP, s->d_next, s->t, n_slots, n_req, rs, rf, og, oi); break;
       default: lanes::k_lanes<8><<<grid, block, 0, s->stream>>>(s->LP, s->d_next, s->t, n_slots, n_req, rs, rf, og, oi); break;
     }
-  } else if (s->use_smem)
-    k_run<true><<<grid, block, s->L.hot_bytes, s->stream>>>(s->P, s->d_next, s->t, n_slots, n_req, rs, rf, og, oi);
-  else
-    k_run<false><<<grid, block, 0, s->stream>>>(s->P, s->d_next, s->t, n_slots, n_req, rs, rf, og, oi);
+  } else {
+    auto* fn = s->use_smem ? (s->L.B > 1 ? k_run<true, true> : k_run<true, false>)
+                           : (s->L.B > 1 ? k_run<false, true> : k_run<false, false>);
+    fn<<<grid, block, s->use_smem ? s->L.hot_bytes : 0, s->stream>>>(s->P, s->d_next, s->t, n_slots, n_req, rs, rf, og, oi);
+  }
   return cuda_check(s, cudaGetLastError(), "k_run launch");
 }
 
@@ -355,30 +356,41 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   if (s->engine == 2) {
     s->threads = 1024;
     s->use_smem = false;
-    if ((rc = cuda_check(s, cudaFuncSetAttribute(k_run_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+    if ((rc = cuda_check(s, cudaFuncSetAttribute(s->L.B > 1 ? k_run_cluster<true> : k_run_cluster<false>,
+                                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                          "cluster attribute")))
       return rc;
     int n_sm = 0;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     int want = n_sm / (cfg->n_scenarios > 0 ? cfg->n_scenarios : 1);
     if (const char* e = getenv("DILU_CLUSTER")) want = atoi(e);
-    int K = want >= 16 ? 16 : (want >= 8 ? 8 : (want >= 4 ? 4 : (want >= 2 ? 2 : 1)));
-    for (; K >= 1; K /= 2) {           // largest cluster the device can schedule
+    // Largest cluster size that keeps every scenario resident in one wave (a cluster of
+    // 16 must fit inside one GPC, so 148 SMs do not always hold 148/16 of them); when no
+    // size does, the one with the fewest waves.
+    const int S = cfg->n_scenarios > 0 ? cfg->n_scenarios : 1;
+    int K = 0, best_waves = 0;
+    for (int k = want >= 16 ? 16 : (want >= 8 ? 8 : (want >= 4 ? 4 : (want >= 2 ? 2 : 1))); k >= 1; k /= 2) {
       cudaLaunchConfig_t lc = {};
-      lc.gridDim = dim3(K);
+      lc.gridDim = dim3(k);
       lc.blockDim = dim3(s->threads);
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = K; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      at[0].val.clusterDim.x = k; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
       lc.attrs = at;
       lc.numAttrs = 1;
       int nclusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&nclusters, k_run_cluster, &lc) == cudaSuccess && nclusters > 0) break;
-      cudaGetLastError();
+      if (cudaOccupancyMaxActiveClusters(&nclusters, s->L.B > 1 ? k_run_cluster<true> : k_run_cluster<false>, &lc) != cudaSuccess || nclusters < 1) {
+        cudaGetLastError();
+        continue;
+      }
+      const int waves = (S + nclusters - 1) / nclusters;
+      if (K == 0 || waves < best_waves) { K = k; best_waves = waves; }
+      if (waves == 1) break;
     }
     if (K < 1) return fail(s, DILU_E_CUDA, "no schedulable cluster size");
     s->K = K;
     s->grid = cfg->n_scenarios * K;
+    if (getenv("DILU_VERBOSE")) fprintf(stderr, "dilu: cluster engine K=%d waves=%d\n", K, best_waves);
     return dilu_sim_reset(s);
   }
   // CTA engine launch shape: one CTA per scenario; hot state in shared memory when it fits
@@ -396,7 +408,8 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   if (const char* e = getenv("DILU_NO_SMEM")) if (atoi(e)) s->use_smem = false;
   if (s->threads > SMEM_MAX_THREADS) s->use_smem = false;
   if (s->use_smem) {
-    if ((rc = cuda_check(s, cudaFuncSetAttribute(k_run<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((rc = cuda_check(s, cudaFuncSetAttribute(s->L.B > 1 ? k_run<true, true> : k_run<true, false>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)s->L.hot_bytes), "smem attribute")))
       return rc;
   }
@@ -404,10 +417,10 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   int per_sm = 0, n_sm = 0;
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   if (s->use_smem)
-    rc = cuda_check(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_run<true>, s->threads,
+    rc = cuda_check(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, s->L.B > 1 ? k_run<true, true> : k_run<true, false>, s->threads,
                                                                      s->L.hot_bytes), "occupancy");
   else
-    rc = cuda_check(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_run<false>, s->threads, 0),
+    rc = cuda_check(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, s->L.B > 1 ? k_run<false, true> : k_run<false, false>, s->threads, 0),
                     "occupancy");
   if (rc) return rc;
   if (per_sm < 1) return fail(s, DILU_E_CUDA, "kernel cannot be resident with %d threads", s->threads);

@@ -46,6 +46,7 @@ constexpr int GSCR = 96;     // u64 words of per-scenario cluster scratch
 struct Acc0 {  // thread-0 tallies, kept in shared memory (not in every thread's registers)
   long long act, memu, rows, pok, pfail, cold, sout, sin, split, maxa;
   long long st[NSTAT];   // statistics: attempts, hope checks, relayouts, events, scanned, slots
+  unsigned long long sum[9];   // end-of-call block sums of the per-thread tallies (Acc)
 };
 enum { S_ATTEMPT = 0, S_HOPE, S_LAYOUT, S_EVENT, S_SCAN, S_SLOT, S_RES, S_FUN };
 struct Acc {   // per-thread tallies
@@ -74,8 +75,7 @@ __device__ __forceinline__ uint64_t mix5(uint32_t scn, uint32_t t, uint32_t i, u
 struct Red {                 // reduction scratch (static shared)
   unsigned long long u64[2][32];
   int32_t i32[2][33];
-  long long acc[10][32];
-  int32_t flag;
+  int32_t flag[2];           // [0] next queue entry / scenario counter, [1] queue length
   int32_t members[64];       // gang member slots of the request being placed
   Acc0 z;
 };
@@ -560,9 +560,12 @@ __device__ int32_t next_attempt(Scn& c, int32_t q, int32_t qn, Acc& acc) {
 // could host it now (gang: the count of hosting GPUs only grows through such g; LLM:
 // the top-4 free memory only grows through such g).  If no such g exists it fails
 // again without rescoring, exactly as the oracle's full rescoring would.
+// Entered without a group barrier after B3 (the leader's serial event pass): only warp 0
+// (which contains the leader) reads the queue before the first barrier below, and it
+// broadcasts the queue length with the first attempt index.
 __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
   View& v = c.v;
-  const int32_t qn = v.h[H_QLEN];
+  int32_t qn = 0;
   bool removed = false;                 // leader only
   int32_t q = 0, prev = -1, prev_placed = 0;
   for (;;) {
@@ -597,9 +600,11 @@ __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
         }
       }
       __syncwarp();
+      if (prev < 0) qn = v.h[H_ERR] ? 0 : v.h[H_QLEN];   // after B3 (same warp)
       const int32_t e = next_attempt(c, q, qn, acc);
       if (c.g.leader()) {
-        *c.flag = e;
+        c.flag[0] = e;
+        c.flag[1] = qn;
         if (e < qn) {                   // gang members, ascending id
           const int32_t n = v.qN[e], f = v.qFunc[e], first = v.qFirst[e];
           int j = 0;
@@ -613,7 +618,8 @@ __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
     }
     c.g.sync();
     TSTOP(17);
-    q = c.g.K == 1 ? *c.flag : __ldcg(c.flag);
+    q = c.g.K == 1 ? c.flag[0] : __ldcg(c.flag);
+    qn = c.g.K == 1 ? c.flag[1] : __ldcg(c.flag + 1);
     if (q >= qn) break;
     const int32_t n = v.qN[q];
     int placed = 0;
@@ -1203,8 +1209,8 @@ __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, int32_t
     for (int32_t f = lo; f < hi && cnt; ++f)
       if (fflag[f]) { v.fList[pos++] = f; --cnt; }
   }
-  const int32_t need_pass = total > 0 || v.h[H_QLEN] > 0;
-  c.g.sync();
+  const int32_t need_pass = total > 0 || v.h[H_QLEN] > 0;   // uniform: QLEN only changes in B3/placement
+  if (total > 0) c.g.sync();                       // the event list is complete before B3
 #ifdef DILU_PHASE_TIMING
   long long bt0 = clock64();
   if (c.g.leader()) acc.z->st[14] -= bt0;   // st[14] += (end of B3) - (end of B1)
@@ -1246,20 +1252,22 @@ __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, int32_t
       else for (int32_t j = 0; j < P.min_inst && !v.h[H_ERR]; ++j) enqueue(c, f, 1);
     }
   }
-  c.g.sync();
 #ifdef DILU_PHASE_TIMING
   if (c.g.leader()) acc.z->st[14] += clock64();
 #endif
-  if (v.h[H_ERR]) return;
-  placement_pass(c, red, ph, t, acc);             // step 5
-  c.g.sync();
+  // step 5.  No barrier between: the pass starts with a warp-0 section (see there).  It
+  // ends with a group barrier after the last commit; what follows it (the leader's queue
+  // compaction) touches only the queue, which nothing reads before the next boundary.
+  placement_pass(c, red, ph, t, acc);
 }
 
 // ---------------------------------------------------------------------------- kernels
 
 // One scenario for one call (scale_step: n_req < 0; place_batch: n_req >= 0), run by a
 // group of K CTAs (K = 1: the calling CTA; K > 1: the calling cluster, crank = CTA rank).
-template <bool SMEM>
+// FUSED: sub-second slots run as fused batches (L.B > 1); a separate instantiation so the
+// one-slot-per-second kernels (C1-C4) carry none of the batch code.
+template <bool SMEM, bool FUSED>
 __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem, int32_t sc, int32_t t0,
                              int32_t n_slots, int32_t n_req, const int32_t* req_scn,
                              const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid,
@@ -1285,7 +1293,7 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
   c.g.gi = reinterpret_cast<int32_t*>(c.g.gu + 32);
   if (K == 1) {
     c.members = red.members;
-    c.flag = &red.flag;
+    c.flag = red.flag;
   } else {
     c.members = reinterpret_cast<int32_t*>(c.g.gu + 48);
     c.flag = reinterpret_cast<int32_t*>(c.g.gu + 80);
@@ -1328,7 +1336,7 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
   } else {
     // ---- dilu_scale_step: the slot loop
     for (int32_t t = t0; t < t0 + n_slots; ++t) {
-      const bool fused = P.L.B > 1;
+      constexpr bool fused = FUSED;
 #ifdef DILU_PHASE_TIMING
       long long tk0 = clock64(), tk1;
 #define TICK(slot) do { tk1 = clock64(); if (c.g.leader()) acc.z->st[8 + (slot)] += tk1 - tk0; tk0 = tk1; } while (0)
@@ -1351,14 +1359,14 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
         }
       }
       if (t % P.SPS == 0) {
-        c.g.sync();                         // P2(t-1) done before state mutates
+        // no barrier here: B1 touches only the per-function window fields, which P2(t-1)
+        // never reads, and B1's own count barrier orders P2(t-1) before B3 mutates state
         TICK(0);
         boundary(c, red, ph, t, acc, pf_ring);
         TICK(1);
         if (v.h[H_ERR]) break;
       }
-      if (v.h[H_DIRTY]) {
-        c.g.sync();
+      if (v.h[H_DIRTY]) {       // set only by boundary work, after >= 1 barrier since P1(t-1)
         rebuild_layout(c);
         if (c.g.leader()) acc.z->st[S_LAYOUT] += 1;
       }
@@ -1411,21 +1419,19 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
 
   // ---- block-reduce the tallies once per call; cluster CTAs merge with atomics
   {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31;
     long long vals[9] = {acc.rtot, acc.rsrv, acc.rvio, acc.iexe, acc.tprg, acc.etot,
                          (long long)acc.hash, acc.nres, acc.nfun};
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
       long long x = vals[q];
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0) red.acc[q][wid] = x;
+      if (lane == 0) atomicAdd(&acc.z->sum[q], (unsigned long long)x);   // mod 2^64 (R8)
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      long long s7[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-      for (int q = 0; q < 9; ++q)
-        for (int k = 0; k < nw; ++k)
-          s7[q] = (long long)((unsigned long long)s7[q] + (unsigned long long)red.acc[q][k]);
+      long long s7[9];
+      for (int q = 0; q < 9; ++q) s7[q] = (long long)acc.z->sum[q];
       long long d[NT];
       d[T_ACT] = acc.z->act;
       d[T_SMU] = acc.z->act * P.T_slot - s7[5];
@@ -1465,7 +1471,7 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
 #endif
 constexpr int SMEM_MAX_THREADS = 256;   // shared-memory variant: <=256 threads, DILU_MINB CTAs/SM
 
-template <bool SMEM>
+template <bool SMEM, bool FUSED>
 __global__ void __launch_bounds__(SMEM ? SMEM_MAX_THREADS : 1024, SMEM ? DILU_MINB : 1)
 k_run(Params Pin, int32_t* next_scn, int32_t t0,
                                               int32_t n_slots, int32_t n_req,
@@ -1477,18 +1483,19 @@ k_run(Params Pin, int32_t* next_scn, int32_t t0,
   __shared__ View sv;
   if (threadIdx.x == 0) sP = Pin;
   for (;;) {
-    if (threadIdx.x == 0) red.flag = atomicAdd(next_scn, 1);
+    if (threadIdx.x == 0) red.flag[0] = atomicAdd(next_scn, 1);
     __syncthreads();
-    const int32_t sc = red.flag;
+    const int32_t sc = red.flag[0];
     __syncthreads();
     if (sc >= sP.S) break;
-    run_scenario<SMEM>(sP, red, sv, smem, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu, out_iid);
+    run_scenario<SMEM, FUSED>(sP, red, sv, smem, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu, out_iid);
   }
 }
 
 // Large scenarios (C3/C5): one thread-block cluster of K CTAs per scenario (cluster
 // dims set at launch, K <= 16), state in HBM/L2; clusters beyond the resident capacity
 // run in waves.  Same device code as k_run through the group abstraction.
+template <bool FUSED>
 __global__ void __launch_bounds__(1024, 1)
 k_run_cluster(Params Pin, int32_t t0, int32_t n_slots, int32_t n_req, const int32_t* req_scn,
               const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid) {
@@ -1502,7 +1509,7 @@ k_run_cluster(Params Pin, int32_t t0, int32_t n_slots, int32_t n_req, const int3
   __syncthreads();
   const int32_t sc = blockIdx.x / csize;
   if (sc >= sP.S) return;   // whole clusters only: uniform across the cluster
-  run_scenario<false>(sP, red, sv, nullptr, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu,
+  run_scenario<false, FUSED>(sP, red, sv, nullptr, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu,
                       out_iid, (int)csize, (int)crank);
 }
 
