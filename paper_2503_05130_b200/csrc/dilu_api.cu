@@ -426,6 +426,9 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   if (per_sm < 1) return fail(s, DILU_E_CUDA, "kernel cannot be resident with %d threads", s->threads);
   const long long cap = (long long)per_sm * n_sm;
   s->grid = (int)(cfg->n_scenarios < cap ? cfg->n_scenarios : cap);
+  if (getenv("DILU_VERBOSE"))
+    fprintf(stderr, "dilu: cta engine threads=%d smem=%d hot=%zu per_sm=%d grid=%d\n", s->threads,
+            (int)s->use_smem, s->L.hot_bytes, per_sm, s->grid);
   if (const char* e = getenv("DILU_GRID")) {   // test/tuning hook: resident scenarios
     const int v = atoi(e);
     if (v >= 1 && v < s->grid) s->grid = v;

@@ -1469,7 +1469,10 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
 #ifndef DILU_MINB
 #define DILU_MINB 3
 #endif
-constexpr int SMEM_MAX_THREADS = 256;   // shared-memory variant: <=256 threads, DILU_MINB CTAs/SM
+#ifndef DILU_SMEM_THREADS
+#define DILU_SMEM_THREADS 256
+#endif
+constexpr int SMEM_MAX_THREADS = DILU_SMEM_THREADS;   // shared-memory variant: <= this many threads, DILU_MINB CTAs/SM
 
 template <bool SMEM, bool FUSED>
 __global__ void __launch_bounds__(SMEM ? SMEM_MAX_THREADS : 1024, SMEM ? DILU_MINB : 1)

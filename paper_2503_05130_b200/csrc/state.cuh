@@ -80,9 +80,10 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B 
   L.fArr = take(4 * (size_t)F); L.fDep = take(4 * (size_t)F); L.fPidx = take(4 * (size_t)F);
   L.fInfL = take(4 * (size_t)F); L.fDefL = take(4 * (size_t)F);
   // serial-path structures the leader walks every boundary (queue, free stack, ...)
-  L.gRel = take(4 * (size_t)G); L.fstack = take(4 * (size_t)I);
-  L.fPrio = take(4 * (size_t)F); L.fCold = take(4 * (size_t)F); L.fLt = take(4 * (size_t)F);
-  L.fK = take(4 * (size_t)F); L.fList = take(4 * (size_t)F);
+  L.gRel = take(4 * (size_t)G);
+  L.fLt = take(4 * (size_t)F); L.fK = take(4 * (size_t)F); L.fList = take(4 * (size_t)F);
+  L.fstack = take(4 * (size_t)I);
+  L.fPrio = take(4 * (size_t)F); L.fCold = take(4 * (size_t)F);
   L.qFunc = take(4 * (size_t)I); L.qFirst = take(4 * (size_t)I); L.qN = take(4 * (size_t)I);
   L.qFail = take(4 * (size_t)I); L.qSlot = take(4 * (size_t)I); L.iQ = take(4 * (size_t)I);
   L.hot_bytes = align16(o);
