@@ -69,8 +69,36 @@ def lib():
                                                 C.c_int32, C.c_int32, C.POINTER(C.c_int32)]
         L.dilu_ref_llm_split.restype = C.c_int32
         L.dilu_ref_llm_split.argtypes = [C.c_int32, P32, P32, P32, P32, P32, P32] + [C.c_int32] * 7 + [P32, P32]
+        L.dilu_ref_alg2_row.restype = None
+        L.dilu_ref_alg2_row.argtypes = [C.c_int32, P32, P32, P32, P32, P64, P32, C.c_int32,
+                                        C.c_int32, P32, P32, P64, P32]
         _lib = L
     return _lib
+
+
+A2_STATES = {0: "NONE", 1: "EMERGENCY", 2: "RECOVERY", 3: "CONTENTION"}
+
+
+def alg2_row(prio, ids, req_p, lim_p, d, cst, NP, p0=0, res_state=None, gpu_state=None):
+    """NP periods of literal Algorithm 2 on one GPU row (dilu_ref_alg2_row).
+    res_state: int32 [n][4] (t_cur, t_min, r_last, last_exec), updated in place;
+    gpu_state: int32 [3] (state, owner, owner_dt), updated in place.
+    Returns (exec [n] int64, grants [NP][n] int32)."""
+    n = len(prio)
+    a = lambda x, t=np.int32: np.ascontiguousarray(np.asarray(x, dtype=t).reshape(-1))
+    if res_state is None:
+        res_state = np.tile(np.array([0, 0, 0, -(1 << 30)], np.int32), (n, 1))
+    if gpu_state is None:
+        gpu_state = np.array([0, -1, 0], np.int32)
+    rs = a(res_state)
+    gs = a(gpu_state)
+    ex = np.zeros(max(n, 1), np.int64)
+    gr = np.zeros(max(NP * n, 1), np.int32)
+    lib().dilu_ref_alg2_row(n, a(prio), a(ids), a(req_p), a(lim_p), a(d, np.int64), a(cst), NP,
+                            p0, rs, gs, ex, gr)
+    res_state[...] = rs.reshape(np.shape(res_state))
+    gpu_state[...] = gs.reshape(np.shape(gpu_state))
+    return ex[:n], gr[:NP * n].reshape(NP, n)
 
 
 class OracleError(RuntimeError):

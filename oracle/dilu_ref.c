@@ -40,12 +40,14 @@ typedef struct {              /* instance i (SURVEY s8(c) "State") */
   int64_t a[MAX_STAGES];      /* tokens allocated this slot, per stage (step 7) */
   int64_t loc[MAX_STAGES];    /* row-local capacity: b_g (INF/LLM) or x (TRAIN)   */
   int32_t warm;               /* placed && ready <= t, evaluated this slot        */
+  ref_a2_res a2[MAX_STAGES];  /* Alg.2 per-stage state (flags bit2), from commit */
 } RInst;
 
 typedef struct {              /* GPU g: R_g, L_g, U_g, res_g (Alg.1)   */
   int32_t R, L, U, nres;
   int32_t res[RES_CAP];       /* instance ids (stage residents); unsorted set    */
   int64_t exec;               /* sum of executed tokens this slot (step 8)       */
+  ref_a2_gpu a2;              /* Alg.2 "state" of this GPU (flags bit2)          */
 } RGpu;
 
 typedef struct {              /* function f: registration, window, live list     */
@@ -243,6 +245,173 @@ void dilu_ref_vertical_row(int32_t n, const int32_t* prio, const int32_t* id,
   free(ord);
 }
 
+/* ------------------------------------- literal Algorithm 2 at 5 ms periods */
+
+/* eta_increase = 1.25 on integer tokens: ceil(max(R_last, 1) * 5 / 4) (D8: the ceiling
+ * and the floor of 1 keep "gradually increased" from sticking at small R). */
+static int32_t a2_grow(int32_t r_last) {
+  int64_t r = r_last < 1 ? 1 : r_last;
+  return (int32_t)((r * 5 + 3) / 4);
+}
+
+/* One GPU row, NP periods (Algorithm 2; P:885-902 workflow).
+ * Each period, in this order:
+ *  0. state bookkeeping (D8): an EMERGENCY whose owner is not a warm resident any more,
+ *     or a row without SLO-sensitive residents, is NONE ("Without collocation").
+ *  1. IssueToken for every SLO-sensitive resident in (prio, id) order (lines 12-24):
+ *     dT = (T_current - T_min) / T_min                                    (line 13)
+ *     dT > eta_violation        -> EMERGENCY, R = MaxTokens * limit        (14-15)
+ *     sum(RW[current]) == 0     -> RECOVERY,  R = MaxTokens * request      (16-17)
+ *     sum(RW[others]) == 0      -> RECOVERY,  R = min(R_last * eta_inc, MaxTokens * limit)
+ *                                                                  (18-19; S:382 min)
+ *     else                      -> CONTENTION, R = MaxTokens * request      (20-21)
+ *     "Only the current instance can reset or modify the EMERGENCY state":
+ *     a non-owner leaves an EMERGENCY in place; a second SLO resident tripping line
+ *     14 takes ownership only with a larger dT.
+ *  2. IssueToken for every best-effort resident in (prio, id) order (lines 25-38):
+ *     NONE -> MaxTokens*limit; EMERGENCY -> min(MaxTokens*request, R_last) / max(dT, 1)
+ *     (S:397 clamp); RECOVERY -> min(R_last*eta_inc, MaxTokens*limit); CONTENTION -> R_last.
+ *  3. Kernel Redirect / drain in (prio, id) order:
+ *     executed = min(pending, R_issue, MaxTokens - executed by earlier residents).
+ *     RW: R_current = executed.  KLC (footnote P:899): a batch's span from the
+ *     start of its first block to the end of its last block, blocks running at the
+ *     resident's rate y = min(R_issue, capacity left) per 5 ms period.
+ *  4. R_last = R_issue.                                                            */
+void dilu_ref_alg2_row(int32_t n, const int32_t* prio, const int32_t* id, const int32_t* req_p,
+                       const int32_t* lim_p, const int64_t* d, const int32_t* cst, int32_t NP,
+                       int32_t p0, ref_a2_res* rs, ref_a2_gpu* gs, int64_t* exec_out,
+                       int32_t* grant_trace) {
+  const int64_t PT = (int64_t)REF_A2_PERIOD_MS * 1000;       /* period length in us */
+  int32_t* ord = (int32_t*)xcalloc((size_t)(n ? n : 1), sizeof(int32_t));
+  int64_t* pending = (int64_t*)xcalloc((size_t)(n ? n : 1), sizeof(int64_t));
+  int64_t* done = (int64_t*)xcalloc((size_t)(n ? n : 1), sizeof(int64_t));
+  int64_t* bstart = (int64_t*)xcalloc((size_t)(n ? n : 1), sizeof(int64_t));
+  int32_t* grant = (int32_t*)xcalloc((size_t)(n ? n : 1), sizeof(int32_t));
+  for (int32_t k = 0; k < n; ++k) {
+    ord[k] = k;
+    pending[k] = d[k];        /* the slot's kernels are queued at its start (D8) */
+    done[k] = 0;              /* tokens executed in this slot */
+    bstart[k] = -1;           /* start time (us, slot-relative) of the batch in progress */
+  }
+  for (int32_t x = 1; x < n; ++x) {  /* insertion sort by (prio, id) */
+    int32_t v = ord[x], y = x - 1;
+    while (y >= 0 && (prio[ord[y]] > prio[v] || (prio[ord[y]] == prio[v] && id[ord[y]] > id[v]))) {
+      ord[y + 1] = ord[y];
+      --y;
+    }
+    ord[y + 1] = v;
+  }
+  for (int32_t p = 0; p < NP; ++p) {
+    const int32_t P = p0 + p;                                /* absolute period */
+    /* 0. state bookkeeping */
+    int32_t any_slo = 0, owner_here = 0;
+    for (int32_t k = 0; k < n; ++k) {
+      if (prio[k] == 0) any_slo = 1;
+      if (id[k] == gs->owner) owner_here = 1;
+    }
+    if (!any_slo || (gs->state == REF_A2_EMERGENCY && !owner_here)) {
+      gs->state = REF_A2_NONE;
+      gs->owner = -1;
+      gs->owner_dt = 0;
+    }
+    /* 1. SLO-sensitive residents */
+    for (int32_t x = 0; x < n; ++x) {
+      int32_t k = ord[x];
+      if (prio[k] != 0) continue;
+      ref_a2_res* r = &rs[k];
+      int64_t dT = r->t_min > 0 ? ((int64_t)r->t_cur - r->t_min) * 1000 / r->t_min : 0;
+      int32_t idle_self = r->last_exec < P - REF_A2_RW;
+      int32_t idle_others = 1;
+      for (int32_t j = 0; j < n; ++j)
+        if (j != k && rs[j].last_exec >= P - REF_A2_RW) idle_others = 0;
+      if (dT > REF_A2_ETA_V) {
+        grant[k] = lim_p[k];
+        if (gs->state != REF_A2_EMERGENCY || gs->owner == id[k] || dT > gs->owner_dt) {
+          gs->state = REF_A2_EMERGENCY;
+          gs->owner = id[k];
+          gs->owner_dt = (int32_t)dT;
+        }
+      } else {
+        int32_t ns;
+        if (idle_self) {
+          ns = REF_A2_RECOVERY;
+          grant[k] = req_p[k];
+        } else if (idle_others) {
+          ns = REF_A2_RECOVERY;
+          int32_t g2 = a2_grow(r->r_last);
+          grant[k] = g2 < lim_p[k] ? g2 : lim_p[k];
+        } else {
+          ns = REF_A2_CONTENTION;
+          grant[k] = req_p[k];
+        }
+        if (gs->state != REF_A2_EMERGENCY || gs->owner == id[k]) {
+          gs->state = ns;
+          gs->owner = -1;
+          gs->owner_dt = 0;
+        }
+      }
+    }
+    /* 2. best-effort residents */
+    for (int32_t x = 0; x < n; ++x) {
+      int32_t k = ord[x];
+      if (prio[k] == 0) continue;
+      ref_a2_res* r = &rs[k];
+      switch (gs->state) {
+        case REF_A2_NONE: grant[k] = lim_p[k]; break;
+        case REF_A2_EMERGENCY: {
+          int64_t m = req_p[k] < r->r_last ? req_p[k] : r->r_last;
+          int64_t div = gs->owner_dt > 1000 ? gs->owner_dt : 1000;   /* max(dT, 1) */
+          grant[k] = (int32_t)(m * 1000 / div);
+          break;
+        }
+        case REF_A2_RECOVERY: {
+          int32_t g2 = a2_grow(r->r_last);
+          grant[k] = g2 < lim_p[k] ? g2 : lim_p[k];
+          break;
+        }
+        default: grant[k] = r->r_last; break;                      /* CONTENTION */
+      }
+    }
+    if (grant_trace)
+      for (int32_t k = 0; k < n; ++k) grant_trace[(int64_t)p * n + k] = grant[k];
+    /* 3. drain with the physical capacity clamp, KLC */
+    int64_t cap = REF_A2_MAX_TOKENS;
+    for (int32_t x = 0; x < n; ++x) {
+      int32_t k = ord[x];
+      ref_a2_res* r = &rs[k];
+      int64_t y = grant[k] < cap ? grant[k] : cap;   /* this period's rate */
+      if (y < 0) y = 0;
+      int64_t ex = pending[k] < y ? pending[k] : y;
+      cap -= ex;
+      if (ex > 0) {
+        r->last_exec = P;
+        if (cst[k] > 0) {
+          /* tokens [a, b) of the slot run this period; token a + j occupies
+           * [p*PT + j*PT/y, p*PT + ceil((j+1)*PT/y)).  Visit every batch m that has a
+           * token here, in order: its start (token m*cst) and its end (token (m+1)*cst-1). */
+          const int64_t a = done[k], b = done[k] + ex, c = cst[k];
+          for (int64_t m = a / c; m * c < b; ++m) {
+            const int64_t first = m * c, last = (m + 1) * c - 1;
+            if (first >= a) bstart[k] = p * PT + (first - a) * PT / y;
+            if (last < b) {
+              const int64_t end = p * PT + ((last - a + 1) * PT + y - 1) / y;
+              const int64_t T = end - bstart[k];
+              r->t_cur = T > INT32_MAX ? INT32_MAX : (int32_t)T;     /* T_current */
+              if (r->t_min == 0 || r->t_cur < r->t_min) r->t_min = r->t_cur;   /* T_min */
+            }
+          }
+        }
+      }
+      pending[k] -= ex;
+      done[k] += ex;
+    }
+    /* 4. */
+    for (int32_t k = 0; k < n; ++k) rs[k].r_last = grant[k];
+  }
+  for (int32_t k = 0; k < n; ++k) exec_out[k] = done[k];
+  free(ord); free(pending); free(done); free(bstart); free(grant);
+}
+
 /* ------------------------------------------------ lazy horizontal scaling */
 
 /* Lazy scale-out/in decision on a full window (Q18, Q19).
@@ -340,6 +509,8 @@ static void commit(RScen* s, int32_t id, int32_t g, int32_t share) {
   RInst* I = &s->inst[id];
   I->g[I->nst] = g;
   I->share[I->nst] = share;
+  ref_a2_res fresh = {0, 0, 0, -(1 << 30)};   /* no KLC recorded, never executed */
+  I->a2[I->nst] = fresh;
   I->nst++;
 }
 
@@ -596,7 +767,7 @@ static void check_invariants(RScen* s, int32_t t) {
       for (int32_t k = 0; k < I->nst; ++k) {
         int64_t rq = (int64_t)F->req_pm * c->slot_ms, lm = (int64_t)F->lim_pm * c->slot_ms;
         if (s->mode == M_EXCLUSIVE) lm = 1000LL * c->slot_ms;   /* pass-through ceiling */
-        if (I->a[k] < rq || I->a[k] > lm)
+        if (I->a[k] < ((c->flags & 4) ? 0 : rq) || I->a[k] > lm)   /* Alg.2: no floor */
           fail(s, REF_E_INVARIANT, "I4 violated: instance %d slot %d", id, t);
       }
   }
@@ -660,7 +831,25 @@ static void slot(RScen* s, int32_t t) {
       }
       ++n;
     }
-    dilu_ref_vertical_row(n, prio, ids, rq, lm, d, T_slot, a);
+    if (c->flags & 4) {
+      /* literal Algorithm 2, slot_ms / 5 periods of 5 ms */
+      int32_t rp[RES_CAP], lp[RES_CAP], cs[RES_CAP];
+      ref_a2_res st[RES_CAP];
+      for (int32_t x = 0; x < n; ++x) {
+        RInst* I = &s->inst[ids[x]];
+        const ref_func* Fn = &s->fn[I->func];
+        rp[x] = (int32_t)(rq[x] / c->slot_ms * REF_A2_PERIOD_MS);   /* req_pm * 5 */
+        lp[x] = (int32_t)(lm[x] / c->slot_ms * REF_A2_PERIOD_MS);   /* lim_pm * 5 (Excl: 5000) */
+        cs[x] = Fn->kind == K_TRAIN ? 0 : (Fn->work_per_batch + I->nst - 1) / I->nst;
+        if (Fn->prio != 0) cs[x] = 0;                           /* KLC only drives SLO residents */
+        st[x] = I->a2[stg[x]];
+      }
+      const int32_t NP = c->slot_ms / REF_A2_PERIOD_MS;
+      dilu_ref_alg2_row(n, prio, ids, rp, lp, d, cs, NP, t * NP, st, &Gp->a2, a, NULL);
+      for (int32_t x = 0; x < n; ++x) s->inst[ids[x]].a2[stg[x]] = st[x];
+    } else {
+      dilu_ref_vertical_row(n, prio, ids, rq, lm, d, T_slot, a);
+    }
     for (int32_t x = 0; x < n; ++x) {
       RInst* I = &s->inst[ids[x]];
       const ref_func* Fn = &s->fn[I->func];
@@ -753,6 +942,7 @@ static int32_t validate(const ref_config* c, const ref_scenario* scen, const ref
   if (c->alpha_w < 0 || c->beta_w < 0 || c->alpha_w > 255 || c->beta_w > 255 ||
       c->alpha_w + c->beta_w == 0) BAD("config: alpha_w/beta_w must be in [0,255], not both 0");
   if (c->slot_ms < 1 || c->slot_ms > 1000 || 1000 % c->slot_ms) BAD("config: slot_ms must divide 1000");
+  if ((c->flags & 4) && c->slot_ms % REF_A2_PERIOD_MS) BAD("config: Alg.2 periods need slot_ms %% 5 == 0");
   if (c->window_s < 1 || c->phi_out < 1 || c->phi_out > c->window_s || c->phi_in < 0 ||
       c->phi_in >= c->window_s || c->phi_out + c->phi_in <= c->window_s)
     BAD("config: need 1<=phi_out<=W, 0<=phi_in<W, phi_out+phi_in>W (S:455)");
@@ -836,6 +1026,7 @@ int32_t dilu_ref_create(const ref_config* cfg, const ref_scenario* scen, const r
       if (sc->mode == M_STATIC_REQUEST) F->lim_pm = F->req_pm;
     }
     sc->gpu = (RGpu*)xcalloc((size_t)cfg->gpus_per_scenario, sizeof(RGpu));
+    for (int32_t g = 0; g < cfg->gpus_per_scenario; ++g) sc->gpu[g].a2.owner = -1;   /* NONE */
     sc->fs = (RFunc*)xcalloc((size_t)cfg->max_funcs, sizeof(RFunc));
     for (int32_t f = 0; f < cfg->max_funcs; ++f)
       sc->fs[f].ring = (int32_t*)xcalloc((size_t)cfg->window_s, sizeof(int32_t));

@@ -40,7 +40,7 @@ typedef struct {
   int32_t n_scenarios, gpus_per_scenario, max_funcs, max_instances;
   int32_t q_pm, mem_mib, omega_pm, gamma_pm, alpha_w, beta_w, slot_ms;
   int32_t window_s, phi_out, phi_in, min_instances, max_residents, max_llm_stages;
-  int32_t n_patterns, pattern_len, flags;           /* flags bit0 LLM split, bit1 invariants */
+  int32_t n_patterns, pattern_len, flags;  /* bit0 LLM split, bit1 invariants, bit2 Alg.2 5 ms */
 } ref_config;
 
 /* mode: 0 Dilu, 1 Exclusive, 2 StaticLimit (MPS-l), 3 StaticRequest (MPS-r),
@@ -72,6 +72,33 @@ int32_t dilu_ref_slot_detail(ref_sim* s, int32_t scenario, int32_t id_cap, int64
                              int32_t* r, int64_t* exec);
 const char* dilu_ref_last_error(const ref_sim* s);
 void dilu_ref_destroy(ref_sim* s);
+
+/* ---- literal Algorithm 2 at 5 ms periods (cfg.flags bit2) ----
+ * Alg.2 IssueToken run per GPU every period ("periodically
+ * (e.g., 5ms)"), with SPEC's vscaler drain and divisor clamp.
+ * Readings (D8): tokens = kernel blocks = per-mille-ms; MaxTokens = 5000 per
+ * 5 ms period; eta_violation = 300 per-mille, eta_increase = 5/4 with a ceiling and a
+ * floor of 1 token, RW = 20 periods; KLC T in microseconds. */
+#define REF_A2_PERIOD_MS 5
+#define REF_A2_MAX_TOKENS 5000
+#define REF_A2_ETA_V 300
+#define REF_A2_RW 20
+enum { REF_A2_NONE = 0, REF_A2_EMERGENCY = 1, REF_A2_RECOVERY = 2, REF_A2_CONTENTION = 3 };
+typedef struct {             /* one stage resident's Alg.2 inputs that persist */
+  int32_t t_cur, t_min;      /* T_current, T_min: last / minimum recorded KLC (us), 0 = none */
+  int32_t r_last;            /* R_last: tokens issued in the previous period */
+  int32_t last_exec;         /* last absolute period with R_current > 0 (sum RW == 0 test) */
+} ref_a2_res;
+typedef struct { int32_t state, owner, owner_dt; } ref_a2_gpu;   /* per-GPU "state" */
+/* NP periods of one GPU row for one slot.  Inputs per warm resident (any order):
+ * prio (0 SLO-sensitive), instance id, per-period request / limit tokens, the slot's
+ * demand d (queued at the slot start), batch size cst (SLO residents; 0 = no KLC).
+ * p0 = absolute index of the slot's first period.  exec_out[k] = tokens executed in
+ * the slot; grant_trace[p*n + k] (optional) = R_issue per period. */
+void dilu_ref_alg2_row(int32_t n, const int32_t* prio, const int32_t* id, const int32_t* req_p,
+                       const int32_t* lim_p, const int64_t* d, const int32_t* cst, int32_t NP,
+                       int32_t p0, ref_a2_res* rs, ref_a2_gpu* gs, int64_t* exec_out,
+                       int32_t* grant_trace);
 
 /* unit steps, exported so tests can pin each one on its own; the loop above calls
  * exactly these functions */
