@@ -82,7 +82,9 @@ typedef struct {
   int32_t max_residents;      /* must be 32                                                */
   int32_t max_llm_stages;     /* 1..4                                             */
   int32_t n_patterns, pattern_len;
-  int32_t flags;              /* bit0: LLM worst-fit split enabled                         */
+  int32_t flags;              /* bit0: LLM worst-fit split enabled; bit2: literal Alg.2 at */
+                              /* 5 ms periods (D8) instead of   */
+                              /* the slot-level grant; needs slot_ms % 5 == 0 (bit1 unused)  */
 } dilu_config;
 
 /* Per-scenario parameters (the C4 sweep varies gamma per scenario). */

@@ -64,6 +64,7 @@ bool check_cfg(const dilu_config* c, char* msg, size_t n) {
       c->alpha_w + c->beta_w == 0)
     BAD("alpha_w, beta_w must be in [0, 255] and not both 0 (R7)");
   if (c->slot_ms < 1 || c->slot_ms > 1000 || 1000 % c->slot_ms != 0) BAD("slot_ms must divide 1000");
+  if ((c->flags & 4) && c->slot_ms % 5 != 0) BAD("Alg.2 periods (flags bit2) need slot_ms %% 5 == 0");
   if (c->window_s < 1 || c->phi_out < 1 || c->phi_out > c->window_s || c->phi_in < 0 ||
       c->phi_in >= c->window_s || c->phi_out + c->phi_in <= c->window_s)
     BAD("window: need 1<=phi_out<=W, 0<=phi_in<W, phi_out+phi_in>W (S:455)");
@@ -130,7 +131,7 @@ int choose_engine(const dilu_config* c) {
     if (!strcmp(v, "cta")) e = 0;
     if (!strcmp(v, "cluster")) e = 2;
     if (!strcmp(v, "lanes") && c->gpus_per_scenario <= 256 && c->max_funcs <= 4096 &&
-        c->max_instances <= 8192)
+        c->max_instances <= 8192 && !(c->flags & 4))     // lanes: no literal Alg.2
       e = 1;
   }
   return e;
@@ -154,6 +155,26 @@ int choose_parts() {
     if (x == 4 || x == 8 || x == 16) p = x;
   }
   return p;
+}
+
+// Kernel variant for a handle: bit0 fused sub-second batches, bit1 literal Alg.2 periods.
+typedef void (*RunFn)(Params, int32_t*, int32_t, int32_t, int32_t, const int32_t*, const int32_t*,
+                      int32_t*, int32_t*);
+typedef void (*ClusterFn)(Params, int32_t, int32_t, int32_t, const int32_t*, const int32_t*,
+                          int32_t*, int32_t*);
+int variant_of(const dilu_config* c, const Layout& L) {
+  return (L.B > 1 ? 1 : 0) | ((c->flags & 4) ? 2 : 0);
+}
+RunFn run_fn(bool smem, int var) {
+  static const RunFn tab[2][4] = {
+      {k_run<false, 0>, k_run<false, 1>, k_run<false, 2>, k_run<false, 3>},
+      {k_run<true, 0>, k_run<true, 1>, k_run<true, 2>, k_run<true, 3>}};
+  return tab[smem ? 1 : 0][var & 3];
+}
+ClusterFn cluster_fn(int var) {
+  static const ClusterFn tab[4] = {k_run_cluster<0>, k_run_cluster<1>, k_run_cluster<2>,
+                                   k_run_cluster<3>};
+  return tab[var & 3];
 }
 
 Carve carve(const dilu_config* c, const Layout& L) {
@@ -230,7 +251,7 @@ dilu_status launch_run(dilu_sim* s, int32_t n_slots, int32_t n_req, const int32_
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    rc = cuda_check(s, cudaLaunchKernelEx(&lc, s->L.B > 1 ? k_run_cluster<true> : k_run_cluster<false>, s->P, s->t, n_slots, n_req, rs, rf, og, oi),
+    rc = cuda_check(s, cudaLaunchKernelEx(&lc, cluster_fn(variant_of(&s->cfg, s->L)), s->P, s->t, n_slots, n_req, rs, rf, og, oi),
                     "k_run_cluster launch");
     if (rc) return rc;
     return cuda_check(s, cudaGetLastError(), "k_run_cluster");
@@ -242,8 +263,7 @@ dilu_status launch_run(dilu_sim* s, int32_t n_slots, int32_t n_req, const int32_
       default: lanes::k_lanes<8><<<grid, block, 0, s->stream>>>(s->LP, s->d_next, s->t, n_slots, n_req, rs, rf, og, oi); break;
     }
   } else {
-    auto* fn = s->use_smem ? (s->L.B > 1 ? k_run<true, true> : k_run<true, false>)
-                           : (s->L.B > 1 ? k_run<false, true> : k_run<false, false>);
+    const RunFn fn = run_fn(s->use_smem, variant_of(&s->cfg, s->L));
     fn<<<grid, block, s->use_smem ? s->L.hot_bytes : 0, s->stream>>>(s->P, s->d_next, s->t, n_slots, n_req, rs, rf, og, oi);
   }
   return cuda_check(s, cudaGetLastError(), "k_run launch");
@@ -257,7 +277,7 @@ size_t dilu_workspace_bytes(const dilu_config* cfg) {
   char msg[256];
   if (!check_cfg(cfg, msg, sizeof msg)) return 0;
   const Layout L = make_layout(cfg->gpus_per_scenario, cfg->max_funcs, cfg->max_instances,
-                               cfg->window_s, choose_batch(cfg));
+                               cfg->window_s, choose_batch(cfg), (cfg->flags & 4) != 0);
   return carve(cfg, L).total;
 }
 
@@ -277,7 +297,7 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   s->cfg = *cfg;
   s->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   s->L = make_layout(cfg->gpus_per_scenario, cfg->max_funcs, cfg->max_instances, cfg->window_s,
-                     choose_batch(cfg));
+                     choose_batch(cfg), (cfg->flags & 4) != 0);
   const Carve k = carve(cfg, s->L);
   if (!d_workspace || ws_bytes < k.total || (reinterpret_cast<uintptr_t>(d_workspace) % ALIGN)) {
     fprintf(stderr, "dilu_sim_create: workspace needs %zu bytes, 256-byte aligned (got %zu)\n",
@@ -356,7 +376,7 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   if (s->engine == 2) {
     s->threads = 1024;
     s->use_smem = false;
-    if ((rc = cuda_check(s, cudaFuncSetAttribute(s->L.B > 1 ? k_run_cluster<true> : k_run_cluster<false>,
+    if ((rc = cuda_check(s, cudaFuncSetAttribute(cluster_fn(variant_of(cfg, s->L)),
                                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                          "cluster attribute")))
       return rc;
@@ -379,7 +399,7 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
       lc.attrs = at;
       lc.numAttrs = 1;
       int nclusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&nclusters, s->L.B > 1 ? k_run_cluster<true> : k_run_cluster<false>, &lc) != cudaSuccess || nclusters < 1) {
+      if (cudaOccupancyMaxActiveClusters(&nclusters, cluster_fn(variant_of(cfg, s->L)), &lc) != cudaSuccess || nclusters < 1) {
         cudaGetLastError();
         continue;
       }
@@ -408,7 +428,7 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   if (const char* e = getenv("DILU_NO_SMEM")) if (atoi(e)) s->use_smem = false;
   if (s->threads > SMEM_MAX_THREADS) s->use_smem = false;
   if (s->use_smem) {
-    if ((rc = cuda_check(s, cudaFuncSetAttribute(s->L.B > 1 ? k_run<true, true> : k_run<true, false>,
+    if ((rc = cuda_check(s, cudaFuncSetAttribute(run_fn(true, variant_of(cfg, s->L)),
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)s->L.hot_bytes), "smem attribute")))
       return rc;
@@ -417,10 +437,10 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   int per_sm = 0, n_sm = 0;
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   if (s->use_smem)
-    rc = cuda_check(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, s->L.B > 1 ? k_run<true, true> : k_run<true, false>, s->threads,
+    rc = cuda_check(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, run_fn(true, variant_of(cfg, s->L)), s->threads,
                                                                      s->L.hot_bytes), "occupancy");
   else
-    rc = cuda_check(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, s->L.B > 1 ? k_run<false, true> : k_run<false, false>, s->threads, 0),
+    rc = cuda_check(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, run_fn(false, variant_of(cfg, s->L)), s->threads, 0),
                     "occupancy");
   if (rc) return rc;
   if (per_sm < 1) return fail(s, DILU_E_CUDA, "kernel cannot be resident with %d threads", s->threads);

@@ -165,6 +165,10 @@ struct Scn {
   int32_t scn_id, om, ga, mode;   // mode: baseline (0 Dilu, 1 Exclusive, 2 MPS-l, 3 MPS-r, 4 eager)
 };
 enum : int32_t { M_DILU = 0, M_EXCLUSIVE = 1, M_STATIC_LIMIT = 2, M_STATIC_REQUEST = 3, M_EAGER = 4 };
+// literal Algorithm 2 at 5 ms periods (cfg.flags bit2; D8)
+enum : int32_t { A2_NONE = 0, A2_EMERGENCY = 1, A2_RECOVERY = 2, A2_CONTENTION = 3 };
+constexpr int32_t A2_PERIOD_MS = 5, A2_MAX_TOKENS = 5000, A2_ETA_V = 300, A2_RW = 20;
+constexpr int32_t A2_NEVER = -(1 << 30);
 
 __device__ __forceinline__ int st_of(int32_t meta) { return meta & 3; }
 __device__ __forceinline__ int nst_of(int32_t meta) { return (meta >> 4) & 7; }
@@ -254,6 +258,10 @@ __device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
   v.iG[s * MAXST + k0] = (int16_t)g;
   v.iShare[s * MAXST + k0] = share;
   if (k0 == 0) v.iSh0[s] = share;
+  if (c.P->flags & 4) {       // Alg.2 stage state starts fresh (D8)
+    const int32_t e = s * MAXST + k0;
+    v.aTc[e] = 0; v.aTm[e] = 0; v.aRl[e] = 0; v.aLe[e] = A2_NEVER;
+  }
   v.iMeta[s] = (meta & ~(7 << 4)) | ((k0 + 1) << 4);
   v.gExcl[g] = 1;             // I* of the request in flight (Q7)
   v.h[H_DIRTY] = 1;
@@ -1109,6 +1117,210 @@ __device__ void phase2_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   }
 }
 
+// ---- literal Algorithm 2 at 5 ms periods (cfg.flags bit2) -------------
+// Replaces P1's one-shot grant: per GPU row (a width-w lane segment, residents in (prio,
+// id) order), slot_ms/5 periods of IssueToken and the drain with the
+// physical capacity clamp, readings DESIGN.md D8.  All per-resident and per-row
+// state stays in registers across the periods; the sequential parts of one period (the
+// per-GPU "state" fold over the SLO residents, the capacity clamp) are segment shuffles.
+// B slots (fused batch) or one slot; r, stage minima and gangs come through base/stride.
+
+__device__ __forceinline__ int32_t a2_grow(int32_t r_last) {   // ceil(max(R_last,1) * 5/4)
+  const long long r = r_last < 1 ? 1 : r_last;
+  return (int32_t)((r * 5 + 3) / 4);
+}
+
+__device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* rbase, size_t rstride,
+                            int32_t* bminb, size_t bstride, int32_t* gangb, size_t gstride,
+                            Acc& acc) {
+  View& v = c.v;
+  const Params& P = *c.P;
+  const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
+  const unsigned FULL = 0xffffffffu;
+  const int32_t* __restrict__ cbase = v.h + H_CBASE;
+  const int32_t* __restrict__ ccnt = v.h + H_CCNT;
+  const int32_t* __restrict__ gbase = v.h + H_GBASE;
+  const int32_t nch = cbase[6];
+  const int32_t NP = P.slot_ms / A2_PERIOD_MS;
+  const long long PT = (long long)A2_PERIOD_MS * 1000;          // period in us
+  const uint64_t hs = sm64((uint32_t)c.scn_id);
+  for (int32_t ch = wid; ch < nch; ch += nwarp) {
+    int k = 0;
+#pragma unroll
+    for (int x = 1; x < 6; ++x) k += (ch >= cbase[x]);
+    const int w = 1 << k;
+    const int j = lane & (w - 1);
+    const int32_t gi = (ch - cbase[k]) * (32 >> k) + (lane >> k);
+    int32_t g = -1, s = -1;
+    if (gi < ccnt[k]) {
+      g = v.gGrow[gbase[k] + gi];
+      if (j < v.gN[g]) s = v.gRes[(size_t)g * RES + j];
+    }
+    // batch-invariant resident fields and its stage's Alg.2 state
+    bool placed = false;
+    int32_t rd = BIG, f = -1, kind = 0, nst = 1, cst = 1, ibs = 1, id = -1, prio = 1;
+    int32_t req_p = 0, lim_p = 0, e = -1;
+    long long dtr = 0;
+    int32_t tc = 0, tm = 0, rl = 0, le = A2_NEVER;
+    if (s >= 0) {
+      const int32_t meta = v.iMeta[s];
+      placed = st_of(meta) == ST_PLACED;
+      if (placed) {
+        rd = v.iReady[s];
+        f = v.iFunc[s];
+        id = v.iId[s];
+        kind = v.fKind[f];
+        prio = v.fPrio[f];
+        nst = nst_of(meta);
+        req_p = v.fReq[f] * A2_PERIOD_MS;
+        lim_p = c.mode == M_EXCLUSIVE ? A2_MAX_TOKENS : v.fLim[f] * A2_PERIOD_MS;
+        if (kind == K_TRAIN) {
+          dtr = v.fDtr[f];
+        } else {
+          ibs = v.fIbs[f];
+          const int32_t cb = v.fCb[f];
+          cst = nst == 1 ? cb : (cb + nst - 1) / nst;
+        }
+        int32_t kst = 0;
+        if (nst > 1) while (v.iG[s * MAXST + kst] != g) ++kst;
+        e = s * MAXST + kst;
+        tc = v.aTc[e]; tm = v.aTm[e]; rl = v.aRl[e]; le = v.aLe[e];
+      }
+    }
+    int32_t st = A2_NONE, ow = -1, odt = 0;          // this row's "state" (replicated)
+    if (g >= 0) { st = v.aSt[g]; ow = v.aOw[g]; odt = v.aDt[g]; }
+    const uint64_t gk = uint64_t((uint32_t)g) << 32;
+    for (int32_t u = 0; u < B; ++u) {
+      const int32_t tu = t + u;
+      const bool warm = placed && rd <= tu;
+      int32_t rr = 0, need = 0;
+      long long dem = 0;                              // the slot's demand, queued at its start
+      if (warm) {
+        if (kind == K_TRAIN) {
+          dem = dtr;
+        } else {
+          rr = rbase[(size_t)u * rstride + s];
+          need = rr / ibs + (rr % ibs != 0);
+          dem = (long long)need * cst;
+        }
+      }
+      const bool slo = warm && prio == 0;
+      const int32_t cklc = slo && kind != K_TRAIN ? cst : 0;
+      long long pend = dem, done = 0, bst = -1;
+      for (int32_t p = 0; p < NP; ++p) {
+        const int32_t Pa = tu * NP + p;
+        // 0. bookkeeping: no SLO resident, or the EMERGENCY owner left -> NONE
+        int32_t nslo = slo, nown = warm && id == ow;
+        const int32_t busy = warm && le >= Pa - A2_RW;
+        int32_t nbusy = busy;
+        for (int o = w >> 1; o > 0; o >>= 1) {
+          nslo += __shfl_xor_sync(FULL, nslo, o, w);
+          nown += __shfl_xor_sync(FULL, nown, o, w);
+          nbusy += __shfl_xor_sync(FULL, nbusy, o, w);
+        }
+        if (nslo == 0 || (st == A2_EMERGENCY && nown == 0)) { st = A2_NONE; ow = -1; odt = 0; }
+        // 1. SLO-sensitive residents (lines 12-24): own grant, proposed state
+        int32_t grant = 0, act = -1, dtv = 0;
+        if (slo) {
+          const long long dT = tm > 0 ? ((long long)tc - tm) * 1000 / tm : 0;
+          if (dT > A2_ETA_V) {
+            grant = lim_p; act = A2_EMERGENCY; dtv = (int32_t)dT;
+          } else if (le < Pa - A2_RW) {
+            grant = req_p; act = A2_RECOVERY;
+          } else if (nbusy - busy == 0) {
+            const int32_t g2 = a2_grow(rl);
+            grant = g2 < lim_p ? g2 : lim_p; act = A2_RECOVERY;
+          } else {
+            grant = req_p; act = A2_CONTENTION;
+          }
+        }
+        // ... the state, folded over them in row order (P:1003 ownership)
+        for (int x = 0; x < w; ++x) {
+          const int32_t ax = __shfl_sync(FULL, act, x, w);
+          const int32_t ix = __shfl_sync(FULL, id, x, w);
+          const int32_t dx = __shfl_sync(FULL, dtv, x, w);
+          if (ax == A2_EMERGENCY) {
+            if (st != A2_EMERGENCY || ow == ix || dx > odt) { st = A2_EMERGENCY; ow = ix; odt = dx; }
+          } else if (ax >= 0) {
+            if (st != A2_EMERGENCY || ow == ix) { st = ax; ow = -1; odt = 0; }
+          }
+        }
+        // 2. best-effort residents (lines 25-38)
+        if (warm && prio != 0) {
+          if (st == A2_NONE) {
+            grant = lim_p;
+          } else if (st == A2_EMERGENCY) {
+            const long long m = req_p < rl ? req_p : rl;
+            grant = (int32_t)(m * 1000 / (odt > 1000 ? odt : 1000));   // max(dT, 1)
+          } else if (st == A2_RECOVERY) {
+            const int32_t g2 = a2_grow(rl);
+            grant = g2 < lim_p ? g2 : lim_p;
+          } else {
+            grant = rl;
+          }
+        }
+        // 3. drain: rate y = min(R_issue, capacity left by earlier residents)
+        const long long q = warm ? (pend < grant ? pend : grant) : 0;
+        long long incl = q;
+        for (int o = 1; o < w; o <<= 1) {
+          const long long yq = __shfl_up_sync(FULL, incl, o, w);
+          if (j >= o) incl += yq;
+        }
+        long long cap = A2_MAX_TOKENS - (incl - q);
+        if (cap < 0) cap = 0;
+        const long long y = grant < cap ? grant : cap;
+        const long long ex = q < cap ? q : cap;
+        if (ex > 0) {
+          le = Pa;
+          if (cklc > 0) {   // KLC: batch spans at rate y (footnote P:899)
+            const long long a0 = done, b0 = done + ex;
+            for (long long m = a0 / cklc; m * cklc < b0; ++m) {
+              const long long first = m * cklc, last = first + cklc - 1;
+              if (first >= a0) bst = p * PT + (first - a0) * PT / y;
+              if (last < b0) {
+                const long long end = p * PT + ((last - a0 + 1) * PT + y - 1) / y;
+                const long long TT = end - bst;
+                tc = TT > 0x7fffffffLL ? 0x7fffffff : (int32_t)TT;
+                if (tm == 0 || tc < tm) tm = tc;
+              }
+            }
+          }
+        }
+        pend -= ex;
+        done += ex;
+        if (warm) rl = grant;                         // 4. R_last
+      }
+      // the slot's results exactly as P1, with a = executed tokens
+      if (warm) {
+        const int32_t a = (int32_t)done;
+        acc.nres += 1;
+        const uint64_t ht = sm64(hs ^ (uint32_t)tu);
+        acc.hash += sm64(sm64(ht ^ (uint32_t)id) ^ (gk | (uint32_t)a));
+        if (kind == K_TRAIN) {
+          const int32_t d = (int32_t)dtr;
+          atomicMin(&gangb[(size_t)u * gstride + f], d < a ? d : a);
+        } else {
+          const int32_t fit = a / cst;
+          const int32_t b = need < fit ? need : fit;
+          if (nst == 1) {
+            const long long capb = (long long)b * ibs;
+            const int32_t served = capb < rr ? (int32_t)capb : rr;
+            acc.rsrv += served;
+            acc.rvio += rr - served;
+            const long long ee = (long long)b * cst;
+            acc.iexe += ee;
+            acc.etot += ee;
+          } else {
+            atomicMin(&bminb[(size_t)u * bstride + s], b);
+          }
+        }
+      }
+    }
+    if (e >= 0) { v.aTc[e] = tc; v.aTm[e] = tm; v.aRl[e] = rl; v.aLe[e] = le; }
+    if (g >= 0 && j == 0) { v.aSt[g] = st; v.aOw[g] = ow; v.aDt[g] = odt; }
+  }
+}
+
 // ---- boundary -----------------------------------------------------------------------
 
 enum : int32_t { EV_DEP = 1, EV_OUT = 2, EV_IN = 4, EV_ARR = 8 };
@@ -1265,9 +1477,10 @@ __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, int32_t
 
 // One scenario for one call (scale_step: n_req < 0; place_batch: n_req >= 0), run by a
 // group of K CTAs (K = 1: the calling CTA; K > 1: the calling cluster, crank = CTA rank).
-// FUSED: sub-second slots run as fused batches (L.B > 1); a separate instantiation so the
-// one-slot-per-second kernels (C1-C4) carry none of the batch code.
-template <bool SMEM, bool FUSED>
+// VAR bit0: sub-second slots run as fused batches (L.B > 1); bit1: literal Alg.2 periods
+// (cfg.flags bit2).  Separate instantiations, so the one-slot-per-second slot-model kernels
+// (C1-C4) carry neither the batch nor the period code.
+template <bool SMEM, int VAR>
 __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem, int32_t sc, int32_t t0,
                              int32_t n_slots, int32_t n_req, const int32_t* req_scn,
                              const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid,
@@ -1336,7 +1549,8 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
   } else {
     // ---- dilu_scale_step: the slot loop
     for (int32_t t = t0; t < t0 + n_slots; ++t) {
-      constexpr bool fused = FUSED;
+      constexpr bool fused = (VAR & 1) != 0;
+      constexpr bool alg2 = (VAR & 2) != 0;
 #ifdef DILU_PHASE_TIMING
       long long tk0 = clock64(), tk1;
 #define TICK(slot) do { tk1 = clock64(); if (c.g.leader()) acc.z->st[8 + (slot)] += tk1 - tk0; tk0 = tk1; } while (0)
@@ -1388,7 +1602,8 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
         }
         c.g.sync();
         TICK(3);
-        phase1_b(c, t, B, acc);
+        if (alg2) phase1_alg2(c, t, B, v.rB, P.I, v.bB, P.I, v.gB, P.F, acc);
+        else phase1_b(c, t, B, acc);
         c.g.sync();
         TICK(4);
         phase2_b(c, t, B, acc);
@@ -1407,7 +1622,12 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
       }
       c.g.sync();
       TICK(3);
-      phase1(c, t, acc);
+      if (alg2) {
+        const int par = t & 1;
+        phase1_alg2(c, t, 1, v.iR + par * P.I, 0, v.iBmin + par * P.I, 0, v.fGang + par * P.F, 0, acc);
+      } else {
+        phase1(c, t, acc);
+      }
       c.g.sync();
       TICK(4);
       phase2(c, t, acc);
@@ -1474,7 +1694,7 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
 #endif
 constexpr int SMEM_MAX_THREADS = DILU_SMEM_THREADS;   // shared-memory variant: <= this many threads, DILU_MINB CTAs/SM
 
-template <bool SMEM, bool FUSED>
+template <bool SMEM, int VAR>
 __global__ void __launch_bounds__(SMEM ? SMEM_MAX_THREADS : 1024, SMEM ? DILU_MINB : 1)
 k_run(Params Pin, int32_t* next_scn, int32_t t0,
                                               int32_t n_slots, int32_t n_req,
@@ -1491,14 +1711,14 @@ k_run(Params Pin, int32_t* next_scn, int32_t t0,
     const int32_t sc = red.flag[0];
     __syncthreads();
     if (sc >= sP.S) break;
-    run_scenario<SMEM, FUSED>(sP, red, sv, smem, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu, out_iid);
+    run_scenario<SMEM, VAR>(sP, red, sv, smem, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu, out_iid);
   }
 }
 
 // Large scenarios (C3/C5): one thread-block cluster of K CTAs per scenario (cluster
 // dims set at launch, K <= 16), state in HBM/L2; clusters beyond the resident capacity
 // run in waves.  Same device code as k_run through the group abstraction.
-template <bool FUSED>
+template <int VAR>
 __global__ void __launch_bounds__(1024, 1)
 k_run_cluster(Params Pin, int32_t t0, int32_t n_slots, int32_t n_req, const int32_t* req_scn,
               const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid) {
@@ -1512,7 +1732,7 @@ k_run_cluster(Params Pin, int32_t t0, int32_t n_slots, int32_t n_req, const int3
   __syncthreads();
   const int32_t sc = blockIdx.x / csize;
   if (sc >= sP.S) return;   // whole clusters only: uniform across the cluster
-  run_scenario<false, FUSED>(sP, red, sv, nullptr, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu,
+  run_scenario<false, VAR>(sP, red, sv, nullptr, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu,
                       out_iid, (int)csize, (int)crank);
 }
 
@@ -1559,6 +1779,8 @@ __global__ void k_init(Params P) {
     v.fGang[f] = BIG; v.fGang[P.F + f] = BIG; v.fFlag[f] = 0; v.fK[f] = 0; v.fList[f] = 0;
     v.fArr[f] = r[11]; v.fDep[f] = r[12]; v.fPidx[f] = 0;
   }
+  if (P.flags & 4)
+    for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) { v.aSt[g] = A2_NONE; v.aOw[g] = -1; v.aDt[g] = 0; }
   if (P.L.B > 1) {
     for (size_t k = threadIdx.x; k < (size_t)P.L.B * P.I; k += blockDim.x) v.bB[k] = BIG;
     for (size_t k = threadIdx.x; k < (size_t)P.L.B * P.F; k += blockDim.x) v.gB[k] = BIG;

@@ -49,12 +49,14 @@ struct Layout {
       fList, fArr, fDep, fPidx, fInfL, fDefL;
   size_t qFunc, qFirst, qN, qFail, qSlot, iQ;
   size_t rB, bB, gB;       // per-batch-slot r, LLM stage minimum, training gang (B > 1 only)
+  size_t aTc, aTm, aRl, aLe, aSt, aOw, aDt;   // literal Alg.2 state (cfg.flags bit2 only)
   size_t hot_bytes, bytes;
 };
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B = 1) {
+inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B = 1,
+                          bool alg2 = false) {
   Layout L;
   L.G = G; L.F = F; L.I = I; L.W = W; L.B = B;
   size_t o = 0;
@@ -96,6 +98,11 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B 
   // boundaries share one placement state, so P0/P1/P2 run once per batch
   const size_t bb = B > 1 ? (size_t)B : 0;
   L.rB = take(4 * bb * I); L.bB = take(4 * bb * I); L.gB = take(4 * bb * F);
+  // literal Algorithm 2 (D8): per stage resident T_current, T_min, R_last,
+  // last executing period [I][MAXST]; per GPU state, owner id, owner dT [G]
+  const size_t ai = alg2 ? (size_t)I * MAXST : 0, ag = alg2 ? (size_t)G : 0;
+  L.aTc = take(4 * ai); L.aTm = take(4 * ai); L.aRl = take(4 * ai); L.aLe = take(4 * ai);
+  L.aSt = take(4 * ag); L.aOw = take(4 * ag); L.aDt = take(4 * ag);
   L.bytes = align16(o);
   return L;
 }
@@ -114,6 +121,7 @@ struct View {
       *fFlag, *fK, *fList, *fArr, *fDep, *fPidx, *fInfL, *fDefL;
   int32_t *qFunc, *qFirst, *qN, *qFail, *qSlot, *iQ;
   int32_t *rB, *bB, *gB;
+  int32_t *aTc, *aTm, *aRl, *aLe, *aSt, *aOw, *aDt;
   int32_t* ring;  // global [F][W]
 };
 
@@ -138,6 +146,7 @@ inline View make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
   P32(fPidx); P32(fInfL); P32(fDefL);
   P32(qFunc); P32(qFirst); P32(qN); P32(qFail); P32(qSlot); P32(iQ);
   P32(rB); P32(bB); P32(gB);
+  P32(aTc); P32(aTm); P32(aRl); P32(aLe); P32(aSt); P32(aOw); P32(aDt);
 #undef P32
   v.ring = nullptr;
   return v;

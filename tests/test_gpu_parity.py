@@ -255,3 +255,46 @@ def test_fused_batches(shape, monkeypatch):
     wl = di.with_modes(di.Workload("C5b", wl.cfg, wl.scen, funcs, wl.patterns, wl.n_slots),
                        [0, 1, 2, 3, 4])
     run_pair(wl, [1, 13, 7, 279, 300], id_cap=16384)
+
+
+# ------------------------------- literal Algorithm 2 at 5 ms periods (s8(f) #2, D8)
+
+def with_alg2(wl):
+    cfg = dict(wl.cfg, flags=wl.cfg["flags"] | 4)
+    return di.Workload(wl.name + "+alg2", cfg, wl.scen, wl.funcs, wl.patterns, wl.n_slots, wl.note)
+
+
+@pytest.mark.parametrize("seed", [0, 3])
+def test_alg2_c2(seed):
+    """C2 with 200 Alg.2 periods per 1 s slot (CTA engine, state in shared memory)."""
+    run_pair(with_alg2(di.c2(seed=seed, T=300)), [1, 119, 180], id_cap=4096)
+
+
+@pytest.mark.parametrize("engine", ["cta", "cluster"])
+def test_alg2_mixed_modes_c4_slice(engine, monkeypatch):
+    """40 C4 sweep points under Alg.2, scenario i in baseline mode i % 5."""
+    monkeypatch.setenv("DILU_ENGINE", engine)
+    wl = di.c4(n_scenarios=4096, T=240).subset(np.arange(3, 4096, 102))
+    wl = with_alg2(di.with_modes(wl, np.arange(wl.S) % 5))
+    run_pair(wl, [1, 239], id_cap=2048)
+
+
+def test_alg2_llm_split():
+    """Alg.2 rows of split LLM instances (stage state per GPU, stage minima in P2)."""
+    wl = with_alg2(di.c4(n_scenarios=4096, T=300).subset(np.arange(0, 640, 61)))
+    gs, rs, tot = run_pair(wl, [300], snap=False)
+    assert tot[T["llm_split_placements"]] > 0
+
+
+@pytest.mark.parametrize("shape", ["cluster_b10", "cta_b10", "cta_b1"])
+def test_alg2_fused_100ms(shape, monkeypatch):
+    """100 ms slots (20 periods each) in fused batches, cold starts ending mid-batch."""
+    engine, _, b = shape.partition("_")
+    monkeypatch.setenv("DILU_ENGINE", engine)
+    monkeypatch.setenv("DILU_BATCH", b[1:])
+    wl = di.scaled("C5b", 512, 60, 120, 360, 100, 400, [53, 54], max_instances=8192)
+    funcs = wl.funcs.copy()
+    live = funcs[:, :, di.FI["kind"]] >= 0
+    funcs[:, :, di.FI["cold_slots"]] += 3 * live
+    wl = with_alg2(di.Workload("C5b", wl.cfg, wl.scen, funcs, wl.patterns, wl.n_slots))
+    run_pair(wl, [1, 13, 186, 200], id_cap=16384)
