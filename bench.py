@@ -41,6 +41,7 @@ OPS_PER_FUNCTION_SLOT = 15      # step 6 for one registered inference function
 OPS_PER_FUNCTION_SECOND = 10    # steps 1 and 3 (window push, counts, decision)
 OPS_PER_GPU_SCORED = 15         # Alg.1 SelectOptGPU per candidate GPU per attempt
 OPS_PER_SCENARIO_SLOT = 6       # fold of active / memory tallies
+OPS_PER_RESIDENT_PERIOD = 30    # --vertical alg2: one resident's IssueToken + drain per 5 ms
 # INT32 issue peak: 148 SMs x (64 ALU-pipe + 64 FMA-pipe lanes)/clk x 1.965 GHz max clock
 # (B300_MICROARCH.md "fma vs alu split ... rt_SMSP=2"; B200_PROFILING.md SM count/clock)
 INT_PEAK_TOPS = 148 * 128 * 1.965e9 / 1e12
@@ -58,10 +59,24 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample scenarios (0: auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--vertical", default="slot", choices=["slot", "alg2"],
+                    help="slot: slot-level grant (default); alg2: literal Algorithm 2 at 5 ms "
+                         "periods (cfg.flags bit2, DESIGN.md D8)")
     return ap.parse_args()
 
 
-def build_workload(name: str, rank: int, world: int, scaling: str, slots: int):
+def build_workload(name: str, rank: int, world: int, scaling: str, slots: int,
+                   vertical: str = "slot"):
+    wl, desc, n = _build_workload(name, rank, world, scaling, slots)
+    if vertical == "alg2":
+        import dilu_inputs as di
+        cfg = dict(wl.cfg, flags=wl.cfg["flags"] | 4)
+        wl = di.Workload(wl.name, cfg, wl.scen, wl.funcs, wl.patterns, wl.n_slots, wl.note)
+        desc += "; literal Alg.2, %d x 5 ms periods per slot" % (wl.cfg["slot_ms"] // 5)
+    return wl, desc, n
+
+
+def _build_workload(name: str, rank: int, world: int, scaling: str, slots: int):
     import dilu_inputs as di
     if name == "C4":
         if scaling == "weak":
@@ -158,7 +173,7 @@ def run_reference(args):
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     if rank != 0:
         return
-    wl, desc, n_slots = build_workload(args.workload, 0, 1, args.scaling, args.slots)
+    wl, desc, n_slots = build_workload(args.workload, 0, 1, args.scaling, args.slots, args.vertical)
     cores = len(os.sched_getaffinity(0))
     sample = args.cpu_sample or max(cores, min(wl.S, 2 * cores))
     vals = []
@@ -189,7 +204,8 @@ def run_dilu(args):
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    wl, desc, n_slots = build_workload(args.workload, rank, world, args.scaling, args.slots)
+    wl, desc, n_slots = build_workload(args.workload, rank, world, args.scaling, args.slots,
+                                        args.vertical)
     sim = DiluSim.from_workload(wl, device=dev)
     stream = sim.stream
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -237,6 +253,8 @@ def run_dilu(args):
            + OPS_PER_FUNCTION_SECOND * stats["function_slots"] // sps
            + OPS_PER_GPU_SCORED * wl.G * stats["attempts"]
            + OPS_PER_SCENARIO_SLOT * stats["slots"])
+    if args.vertical == "alg2":
+        ops += OPS_PER_RESIDENT_PERIOD * stats["resident_slots"] * (wl.cfg["slot_ms"] // 5)
     k_s = sum(kern_ms) / len(kern_ms) / 1000.0
     achieved = ops / k_s / 1e12
     traffic = None
@@ -287,7 +305,7 @@ def run_dilu(args):
             "config": {"workload": desc, "scenarios_per_gpu": wl.S, "gpus_per_scenario": wl.G,
                        "slots": n_slots, "slot_ms": wl.cfg["slot_ms"], "decisions_per_step": D_all,
                        "l2": "flushed between timed steps (256 MiB write)",
-                       "parallelism": f"scenario shards x{world}"},
+                       "parallelism": f"scenario shards x{world}", "vertical": args.vertical},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": INT_PEAK_TOPS,
                          "unit": "Tops/s", "frac": achieved / INT_PEAK_TOPS, "traffic": traffic,
                          "kernel": "k_run (one launch per step)", "kernel_ms": 1000 * k_s,

@@ -1206,23 +1206,21 @@ __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* rbase, 
       }
       const bool slo = warm && prio == 0;
       const int32_t cklc = slo && kind != K_TRAIN ? cst : 0;
-      long long pend = dem, done = 0, bst = -1;
+      long long pend = dem;
+      int32_t done = 0, bst = -1;                     // slot-relative: <= slot_ms * 1000
+      long long dT = tm > 0 ? ((long long)tc - tm) * 1000 / tm : 0;   // changes with tc, tm only
       for (int32_t p = 0; p < NP; ++p) {
         const int32_t Pa = tu * NP + p;
-        // 0. bookkeeping: no SLO resident, or the EMERGENCY owner left -> NONE
-        int32_t nslo = slo, nown = warm && id == ow;
+        // 0. bookkeeping: no SLO resident, or the EMERGENCY owner left -> NONE.  One
+        // segment sum of three packed counts (each <= 32): SLO, owner, busy (RW != 0)
         const int32_t busy = warm && le >= Pa - A2_RW;
-        int32_t nbusy = busy;
-        for (int o = w >> 1; o > 0; o >>= 1) {
-          nslo += __shfl_xor_sync(FULL, nslo, o, w);
-          nown += __shfl_xor_sync(FULL, nown, o, w);
-          nbusy += __shfl_xor_sync(FULL, nbusy, o, w);
-        }
+        int32_t cnt = (int32_t)slo | ((int32_t)(warm && id == ow) << 8) | (busy << 16);
+        for (int o = w >> 1; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o, w);
+        const int32_t nslo = cnt & 0xff, nown = (cnt >> 8) & 0xff, nbusy = cnt >> 16;
         if (nslo == 0 || (st == A2_EMERGENCY && nown == 0)) { st = A2_NONE; ow = -1; odt = 0; }
         // 1. SLO-sensitive residents (lines 12-24): own grant, proposed state
         int32_t grant = 0, act = -1, dtv = 0;
         if (slo) {
-          const long long dT = tm > 0 ? ((long long)tc - tm) * 1000 / tm : 0;
           if (dT > A2_ETA_V) {
             grant = lim_p; act = A2_EMERGENCY; dtv = (int32_t)dT;
           } else if (le < Pa - A2_RW) {
@@ -1234,11 +1232,19 @@ __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* rbase, 
             grant = req_p; act = A2_CONTENTION;
           }
         }
-        // ... the state, folded over them in row order (P:1003 ownership)
-        for (int x = 0; x < w; ++x) {
-          const int32_t ax = __shfl_sync(FULL, act, x, w);
-          const int32_t ix = __shfl_sync(FULL, id, x, w);
-          const int32_t dx = __shfl_sync(FULL, dtv, x, w);
+        // ... the state, folded over them in row order (P:1003 ownership): visit
+        // the segment's SLO lanes in order (the warp iterates max-over-segments times)
+        const unsigned seg = (w == 32 ? FULL : ((1u << w) - 1)) << (lane & ~(w - 1));
+        unsigned todo = __ballot_sync(FULL, act >= 0) & seg;
+        const int nrounds = __reduce_max_sync(FULL, __popc(todo));
+        for (int x = 0; x < nrounds; ++x) {
+          const bool have = todo != 0;              // this segment still has an SLO lane
+          const int src = have ? __ffs(todo) - 1 : lane;
+          todo &= todo - 1;
+          const int32_t axs = __shfl_sync(FULL, act, src);
+          const int32_t ax = have ? axs : -1;
+          const int32_t ix = __shfl_sync(FULL, id, src);
+          const int32_t dx = __shfl_sync(FULL, dtv, src);
           if (ax == A2_EMERGENCY) {
             if (st != A2_EMERGENCY || ow == ix || dx > odt) { st = A2_EMERGENCY; ow = ix; odt = dx; }
           } else if (ax >= 0) {
@@ -1272,22 +1278,24 @@ __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* rbase, 
         const long long ex = q < cap ? q : cap;
         if (ex > 0) {
           le = Pa;
-          if (cklc > 0) {   // KLC: batch spans at rate y (footnote P:899)
-            const long long a0 = done, b0 = done + ex;
-            for (long long m = a0 / cklc; m * cklc < b0; ++m) {
-              const long long first = m * cklc, last = first + cklc - 1;
-              if (first >= a0) bst = p * PT + (first - a0) * PT / y;
+          if (cklc > 0) {   // KLC: batch spans at rate y (footnote P:899); 32-bit: spans and
+                            // offsets are within the slot, (token offset) * 5000 <= 2.5e7
+            const int32_t a0 = done, b0 = done + (int32_t)ex, yy = (int32_t)y, pt = (int32_t)PT;
+            bool upd = false;
+            for (int32_t m = a0 / cklc; m * cklc < b0; ++m) {
+              const int32_t first = m * cklc, last = first + cklc - 1;
+              if (first >= a0) bst = p * pt + (first - a0) * pt / yy;
               if (last < b0) {
-                const long long end = p * PT + ((last - a0 + 1) * PT + y - 1) / y;
-                const long long TT = end - bst;
-                tc = TT > 0x7fffffffLL ? 0x7fffffff : (int32_t)TT;
+                tc = p * pt + ((last - a0 + 1) * pt + yy - 1) / yy - bst;
                 if (tm == 0 || tc < tm) tm = tc;
+                upd = true;
               }
             }
+            if (upd) dT = ((long long)tc - tm) * 1000 / tm;
           }
         }
         pend -= ex;
-        done += ex;
+        done += (int32_t)ex;
         if (warm) rl = grant;                         // 4. R_last
       }
       // the slot's results exactly as P1, with a = executed tokens
