@@ -20,11 +20,11 @@ NT = 17
 
 
 def build(force: bool = False) -> str:
-    src = os.path.join(_HERE, "dilu_ref.c")
+    srcs = [os.path.join(_HERE, n) for n in ("dilu_ref.c", "dilu_ref_profile.c")]
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
-            os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "dilu_ref.h"))):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", "-pthread",
-                               src, "-o", LIB_PATH])
+            [os.path.getmtime(x) for x in srcs] + [os.path.getmtime(os.path.join(_HERE, "dilu_ref.h"))]):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-Wall", "-shared",
+                               "-fPIC", "-pthread"] + srcs + ["-lm", "-o", LIB_PATH])
     return LIB_PATH
 
 
@@ -69,6 +69,12 @@ def lib():
                                                 C.c_int32, C.c_int32, C.POINTER(C.c_int32)]
         L.dilu_ref_llm_split.restype = C.c_int32
         L.dilu_ref_llm_split.argtypes = [C.c_int32, P32, P32, P32, P32, P32, P32] + [C.c_int32] * 7 + [P32, P32]
+        L.dilu_ref_profile_batch.restype = None
+        L.dilu_ref_profile_batch.argtypes = [C.c_int32, C.c_void_p, C.c_void_p]
+        L.dilu_ref_infer_exec_ms.restype = C.c_double
+        L.dilu_ref_infer_exec_ms.argtypes = [C.c_void_p, C.c_int32, C.c_double]
+        L.dilu_ref_train_tput.restype = C.c_double
+        L.dilu_ref_train_tput.argtypes = [C.c_void_p, C.c_double]
         L.dilu_ref_alg2_row.restype = None
         L.dilu_ref_alg2_row.argtypes = [C.c_int32, P32, P32, P32, P32, P64, P32, C.c_int32,
                                         C.c_int32, P32, P32, P64, P32]
@@ -184,3 +190,25 @@ def run(wl, n_slots: Optional[int] = None, threads: int = 1, flags: Optional[int
     out = s.metrics()
     s.close()
     return out
+
+
+def profile_batch(sessions):
+    """The profiler oracle over a ``dilu_inputs.PROF_SESSION`` array; returns a
+    ``dilu_inputs.PROF_OUT`` array (SURVEY s8(f) #3)."""
+    import dilu_inputs as di
+    ses = np.ascontiguousarray(sessions, dtype=di.PROF_SESSION)
+    out = np.zeros(len(ses), dtype=di.PROF_OUT)
+    lib().dilu_ref_profile_batch(len(ses), ses.ctypes.data, out.ctypes.data)
+    return out
+
+
+def infer_exec_ms(session, ibs: int, smr: float) -> float:
+    import dilu_inputs as di
+    s = np.ascontiguousarray(np.asarray(session, dtype=di.PROF_SESSION).reshape(1))
+    return lib().dilu_ref_infer_exec_ms(s.ctypes.data, ibs, smr)
+
+
+def train_tput(session, smr: float) -> float:
+    import dilu_inputs as di
+    s = np.ascontiguousarray(np.asarray(session, dtype=di.PROF_SESSION).reshape(1))
+    return lib().dilu_ref_train_tput(s.ctypes.data, smr)

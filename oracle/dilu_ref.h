@@ -120,6 +120,31 @@ int32_t dilu_ref_llm_split(int32_t n_gpu, const int32_t* active, const int32_t* 
                            int32_t omega_u, int32_t gamma_u, int32_t M, int32_t max_stages,
                            int32_t* out_g, int32_t* out_share);
 
+/* ---- batched profiler (PAPER.md:604-639 s3.2) ----
+ * dilu_ref_profile.c.  fp64 throughout (the paper fixes no precision); no FMA
+ * contraction (built with -ffp-contract=off) so every rounding is the plain IEEE one. */
+typedef struct {
+  int32_t kind;        /* 0 inference (Hybrid Growth Search), 2 training (bisection)     */
+  int32_t workers;     /* training: data-parallel workers                                 */
+  int32_t ibs_max;     /* inference: largest IBS of the doubling grid (32: 6 levels)      */
+  int32_t reserved;
+  double a_ms, b_ms, knee_c;   /* inference latency model                    */
+  double knee_t, t_max, idle;  /* training throughput model                  */
+  double slo_ms, smr_step;     /* inference: SLO (t_exec budget SLO/2), SMR growth */
+  double p_req, p_lim, tol;    /* training: p = 0.8 / 1.0, +-2 %              */
+} ref_prof_session;
+typedef struct {
+  double request_smr, limit_smr;   /* SM rate in percent                                 */
+  double t_exec_ms;                /* inference: exec time at <IBS, request>; training: T1 */
+  int32_t ibs, trials;             /* chosen IBS (inference), perfmodel evaluations        */
+  int32_t req_pm, lim_pm;          /* Q25 loader rounding of the two quotas                */
+  int32_t status, reserved;        /* 0 ok, 1 SLO unattainable, 2 non-monotone oracle      */
+} ref_prof_out;
+double dilu_ref_infer_exec_ms(const ref_prof_session* m, int32_t ibs, double smr);
+double dilu_ref_train_tput(const ref_prof_session* m, double smr);
+void dilu_ref_profile_one(const ref_prof_session* in, ref_prof_out* out);
+void dilu_ref_profile_batch(int32_t n, const ref_prof_session* in, ref_prof_out* out);
+
 #ifdef __cplusplus
 }
 #endif
