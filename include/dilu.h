@@ -185,6 +185,38 @@ const char* dilu_last_error(const dilu_sim* s);
 /* Release the handle (not the caller-owned workspace or stream). */
 void dilu_sim_destroy(dilu_sim* s);
 
+/* ---- batched profiler: the step before the loop ------------------
+ * Multi-factor profiling of PAPER.md s3.2 over SPEC's synthetic perfmodel
+ * (the paper measures real GPUs): training quotas by bisection,
+ * inference <IBS, SMR> by the Hybrid Growth Search, one thread per session.
+ * fp64 with plain IEEE operations (no contraction); readings DESIGN.md D9.  The output
+ * rows carry the Q25-rounded per-mille quotas the loop's dilu_func rows take. */
+typedef struct {
+  int32_t kind;        /* 0 inference (Hybrid Growth Search), 2 training (bisection)     */
+  int32_t workers;     /* training: data-parallel workers (>= 1)                          */
+  int32_t ibs_max;     /* inference: largest IBS of the doubling grid, 1..1024 (32 = 6 levels) */
+  int32_t reserved;    /* 0 */
+  double a_ms, b_ms, knee_c;   /* inference t_exec = (a + b*IBS)*knee/min(SMR, knee),     */
+                               /* knee = min(100, knee_c*sqrt(IBS))            */
+  double knee_t, t_max, idle;  /* training throughput = workers*t_max*min(1, SMR/knee_t)*(1-idle) */
+  double slo_ms, smr_step;     /* inference: SLO (t_exec budget SLO/2), SMR step (10) */
+  double p_req, p_lim, tol;    /* training: 0.8, 1.0, 0.02                     */
+} dilu_prof_session;           /* 104 bytes */
+typedef struct {
+  double request_smr, limit_smr;   /* percent                                             */
+  double t_exec_ms;                /* inference: t_exec at <IBS, request>; training: T1    */
+  int32_t ibs, trials;             /* chosen IBS (0 for training); perfmodel evaluations   */
+  int32_t req_pm, lim_pm;          /* ceil(10*percent), limit capped at 1000 (Q25)         */
+  int32_t status, reserved;        /* 0 ok, 1 SLO unattainable, 2 non-monotone throughput  */
+} dilu_prof_out;                   /* 48 bytes */
+
+/* Profile n sessions: d_sessions[n] in, d_out[n] out (device memory, 8-byte aligned),
+ * stream-ordered and asynchronous on cuda_stream.  Returns DILU_E_USAGE for n < 0 or
+ * null pointers with n > 0, DILU_E_CUDA on a launch error; per-session failures are
+ * d_out[i].status, not call errors.  No handle needed. */
+dilu_status dilu_profile(const dilu_prof_session* d_sessions, int32_t n, dilu_prof_out* d_out,
+                         void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

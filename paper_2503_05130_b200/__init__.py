@@ -60,6 +60,8 @@ def lib():
         L.dilu_last_error.argtypes = [vp]
         L.dilu_sim_destroy.restype = None
         L.dilu_sim_destroy.argtypes = [vp]
+        L.dilu_profile.restype = i32
+        L.dilu_profile.argtypes = [vp, i32, vp, vp]
         _lib = L
     return _lib
 
@@ -67,7 +69,7 @@ def lib():
 EXPORTED = ["dilu_workspace_bytes", "dilu_sim_create", "dilu_sim_reset", "dilu_place_batch",
             "dilu_scale_step", "dilu_metrics", "dilu_snapshot", "dilu_kernel_stats",
             "dilu_current_slot",
-            "dilu_last_error", "dilu_sim_destroy"]
+            "dilu_last_error", "dilu_sim_destroy", "dilu_profile"]
 
 
 def _i32(a) -> np.ndarray:
@@ -185,3 +187,27 @@ class DiluSim:
             self.close()
         except Exception:
             pass
+
+
+PROF_SESSION_BYTES, PROF_OUT_BYTES = 104, 48
+
+
+def dilu_profile(sessions, out=None, stream=None):
+    """Batched profiler (dilu_profile).  ``sessions``: a uint8 CUDA tensor
+    of n * 104 bytes (rows laid out as dilu_prof_session, e.g. a dilu_inputs.PROF_SESSION
+    array copied to the device); returns (or fills) a uint8 CUDA tensor of n * 48 bytes
+    (dilu_prof_out rows).  Asynchronous on ``stream`` (default: the current stream)."""
+    import torch
+    if not (isinstance(sessions, torch.Tensor) and sessions.is_cuda and sessions.dtype == torch.uint8):
+        raise TypeError("sessions must be a uint8 CUDA tensor of dilu_prof_session rows")
+    n = sessions.numel() // PROF_SESSION_BYTES
+    if sessions.numel() != n * PROF_SESSION_BYTES:
+        raise ValueError("sessions size is not a multiple of 104 bytes")
+    if out is None:
+        out = torch.empty(n * PROF_OUT_BYTES, dtype=torch.uint8, device=sessions.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(sessions.device)
+    rc = lib().dilu_profile(sessions.data_ptr(), n, out.data_ptr(), stream.cuda_stream)
+    if rc:
+        raise DiluError(rc, "dilu_profile failed")
+    return out

@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libdilu.so")
-SOURCES = [os.path.join(HERE, "csrc", n) for n in ("dilu_api.cu", "sim_kernel.cuh", "state.cuh")]
+SOURCES = [os.path.join(HERE, "csrc", n) for n in ("dilu_api.cu", "sim_kernel.cuh", "state.cuh", "sim_lanes.cuh", "profile.cuh")]
 HEADER = os.path.join(ROOT, "include", "dilu.h")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xptxas", "-v", "-shared", "-Xcompiler", "-fPIC"]

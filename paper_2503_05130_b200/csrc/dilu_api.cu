@@ -16,6 +16,7 @@
 #include "../../include/dilu.h"
 #include "sim_kernel.cuh"
 #include "sim_lanes.cuh"
+#include "profile.cuh"
 
 using namespace dilu;
 
@@ -570,5 +571,21 @@ int32_t dilu_current_slot(const dilu_sim* s) { return s ? s->t : -1; }
 const char* dilu_last_error(const dilu_sim* s) { return s ? s->err : "null handle"; }
 
 void dilu_sim_destroy(dilu_sim* s) { delete s; }
+
+dilu_status dilu_profile(const dilu_prof_session* d_sessions, int32_t n, dilu_prof_out* d_out,
+                         void* cuda_stream) {
+  if (n < 0 || (n > 0 && (!d_sessions || !d_out))) return DILU_E_USAGE;
+  if ((reinterpret_cast<uintptr_t>(d_sessions) | reinterpret_cast<uintptr_t>(d_out)) & 7)
+    return DILU_E_USAGE;
+  if (n == 0) return DILU_OK;
+  int dev = 0, n_sm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const int per = 8;                          // resident 256-thread CTAs per SM (regs permitting)
+  long long blocks = (n + 255) / 256;
+  if (blocks > (long long)n_sm * per) blocks = (long long)n_sm * per;
+  prof::k_profile<<<(int)blocks, 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(d_sessions, n, d_out);
+  return cudaGetLastError() == cudaSuccess ? DILU_OK : DILU_E_CUDA;
+}
 
 }  // extern "C"
