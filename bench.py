@@ -53,7 +53,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dilu", choices=["dilu", "reference"])
-    ap.add_argument("--workload", default="C4", choices=["C4", "C2", "C3", "C5"])
+    ap.add_argument("--workload", default="C4", choices=["C4", "C2", "C3", "C5", "PROFILE"],
+                    help="PROFILE: the batched profiler (SURVEY 8(f) #3) over the C4 sweep's "
+                         "4,096 x 200 function rows, metric profiling sessions/s")
+    ap.add_argument("--prof-sessions", type=int, default=4096 * 200)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--slots", type=int, default=0, help="slots per step (0: workload default)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample scenarios (0: auto)")
@@ -321,9 +324,124 @@ def run_dilu(args):
     ddist.barrier()
 
 
+PROF_METRIC, PROF_UNIT = "profiling sessions/sec", "sessions/s"
+PROF_BYTES_PER_SESSION = 104 + 48       # one dilu_prof_session read + one dilu_prof_out written
+
+
+def run_profile(args):
+    """The batched profiler: one dilu_profile launch per step over the C4 sweep's function
+    rows (weak scaling: every rank profiles its own replica)."""
+    import numpy as np
+    import dilu_inputs as di
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    n = args.prof_sessions
+    ses = di.profile_sessions(n, seed=1000 + rank)
+    cores = len(os.sched_getaffinity(0))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        import oracle
+        sub = ses[: min(n, 2_000_000)]
+        times = []
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            oracle.profile_batch(sub)
+            if k >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        v = len(sub) * len(times) / sum(times)
+        line = {"impl": "reference", "metric": PROF_METRIC, "value": v, "unit": PROF_UNIT,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "profiler over %d C4-sweep function rows" % len(sub)},
+                "cpu_baseline": {"value": v, "unit": PROF_UNIT, "cores": 1, "kind": "oracle",
+                                 "sample": "%d sessions, one thread" % len(sub)},
+                "e2e": {"value": v, "unit": PROF_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    import torch
+    from paper_2503_05130_b200 import dilu_profile, dist as ddist
+    rank, world = ddist.init("nccl")
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    host = torch.from_numpy(np.ascontiguousarray(ses).view(np.uint8)).pin_memory()
+    d_in = host.to(dev)
+    d_out = torch.empty(n * 48, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        dilu_profile(d_in, d_out)
+    torch.cuda.synchronize()
+    ms = []
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            torch.cuda.synchronize()
+            ddist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dilu_profile(d_in, d_out)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        ddist.barrier()
+    max_ms = ddist.allreduce_max(sum(ms))
+    value = n * world * args.steps / (max_ms / 1000.0)
+    k_s = sum(ms) / len(ms) / 1000.0
+    achieved = n * PROF_BYTES_PER_SESSION / k_s / 1e9
+    try:
+        peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        src = "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        peak, src = 7700.0, "B200_PROFILING.md fallback"
+    # end to end: pinned host sessions -> device -> profile -> outputs back to pinned host
+    h_out = torch.empty(n * 48, dtype=torch.uint8).pin_memory()
+    times = []
+    for k in range(max(1, args.e2e_steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d2 = host.to(dev, non_blocking=True)
+        o2 = dilu_profile(d2)
+        h_out.copy_(o2, non_blocking=True)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    e2e_s = ddist.allreduce_max(sum(times))
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        sub = ses[: min(n, 1_000_000)]
+        t0 = time.perf_counter()
+        oracle.profile_batch(sub)
+        dt = time.perf_counter() - t0
+        cpu = {"value": len(sub) / dt, "unit": PROF_UNIT, "cores": 1, "kind": "oracle",
+               "sample": "%d sessions, one thread, %.2f s" % (len(sub), dt)}
+    if rank == 0:
+        line = {"metric": PROF_METRIC, "value": value, "unit": PROF_UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": "profiler (SURVEY 8(f) #3) over %d C4-sweep function rows "
+                                       "per GPU (3/4 inference HGS, 1/4 training bisection)" % n,
+                           "sessions_per_gpu": n, "l2": "flushed between timed steps (256 MiB write)",
+                           "parallelism": f"session shards x{world}"},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": None, "kernel": "k_profile",
+                             "kernel_ms": 1000 * k_s, "bytes_per_session": PROF_BYTES_PER_SESSION,
+                             "peak_source": src},
+                "cpu_baseline": cpu,
+                "e2e": {"value": n * world * len(times) / e2e_s, "unit": PROF_UNIT,
+                        "h2d_bytes_per_step": n * 104, "d2h_bytes_per_step": n * 48},
+                "gpu_launches": args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    ddist.barrier()
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.workload == "PROFILE":
+        run_profile(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_dilu(args)
