@@ -69,6 +69,12 @@ def lib():
                                                 C.c_int32, C.c_int32, C.POINTER(C.c_int32)]
         L.dilu_ref_llm_split.restype = C.c_int32
         L.dilu_ref_llm_split.argtypes = [C.c_int32, P32, P32, P32, P32, P32, P32] + [C.c_int32] * 7 + [P32, P32]
+        L.dilu_ref_latency.restype = C.c_int32
+        L.dilu_ref_latency.argtypes = [C.c_void_p, P64, P64]
+        L.dilu_ref_lat_bucket.restype = C.c_int32
+        L.dilu_ref_lat_bucket.argtypes = [C.c_int64]
+        L.dilu_ref_instance_latency.restype = None
+        L.dilu_ref_instance_latency.argtypes = [C.c_int64] * 6 + [P64]
         L.dilu_ref_profile_batch.restype = None
         L.dilu_ref_profile_batch.argtypes = [C.c_int32, C.c_void_p, C.c_void_p]
         L.dilu_ref_infer_exec_ms.restype = C.c_double
@@ -105,6 +111,9 @@ def alg2_row(prio, ids, req_p, lim_p, d, cst, NP, p0=0, res_state=None, gpu_stat
     res_state[...] = rs.reshape(np.shape(res_state))
     gpu_state[...] = gs.reshape(np.shape(gpu_state))
     return ex[:n], gr[:NP * n].reshape(NP, n)
+
+
+NLAT = 82
 
 
 class OracleError(RuntimeError):
@@ -152,6 +161,13 @@ class RefSim:
         per = np.zeros((self.wl.S, NT), dtype=np.int64)
         tot = np.zeros(NT, dtype=np.int64)
         self._check(lib().dilu_ref_metrics(self.h, per.reshape(-1), tot))
+        return per, tot
+
+    def latency(self) -> Tuple[np.ndarray, np.ndarray]:
+        """Request-level latency vectors [S][82] and their sum (cfg.flags bit3)."""
+        per = np.zeros((self.wl.S, NLAT), dtype=np.int64)
+        tot = np.zeros(NLAT, dtype=np.int64)
+        self._check(lib().dilu_ref_latency(self.h, per.reshape(-1), tot))
         return per, tot
 
     def snapshot(self, id_cap: int) -> Tuple[np.ndarray, np.ndarray]:
@@ -212,3 +228,13 @@ def train_tput(session, smr: float) -> float:
     import dilu_inputs as di
     s = np.ascontiguousarray(np.asarray(session, dtype=di.PROF_SESSION).reshape(1))
     return lib().dilu_ref_train_tput(s.ctypes.data, smr)
+
+
+def lat_bucket(L: int) -> int:
+    return int(lib().dilu_ref_lat_bucket(int(L)))
+
+
+def instance_latency(r, ibs, b, e, slo_us, T_us):
+    lat = np.zeros(NLAT, dtype=np.int64)
+    lib().dilu_ref_instance_latency(int(r), int(ibs), int(b), int(e), int(slo_us), int(T_us), lat)
+    return lat

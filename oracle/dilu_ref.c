@@ -70,6 +70,8 @@ typedef struct {
   int32_t n_ids, cap_ids, n_live;
   RReq* q; int32_t nq, cap_q;  /* FIFO queue (Q9) */
   int64_t tally[REF_NT];
+  int64_t lat[REF_NLAT];       /* request-level latency vector (flags bit3) */
+  int64_t* slo_us;             /* [F] SLO of each inference function (D10) */
   int32_t err;
   char msg[200];
 } RScen;
@@ -410,6 +412,51 @@ void dilu_ref_alg2_row(int32_t n, const int32_t* prio, const int32_t* id, const 
   }
   for (int32_t k = 0; k < n; ++k) exec_out[k] = done[k];
   free(ord); free(pending); free(done); free(bstart); free(grant);
+}
+
+/* ------------------------------------------------ request-level latency */
+
+/* Log-spaced latency buckets, 4 per octave (D10). */
+int32_t dilu_ref_lat_bucket(int64_t L) {
+  if (L < 4) return (int32_t)(L < 0 ? 0 : L);
+  int32_t h = 0;
+  while ((L >> (h + 1)) != 0) ++h;               /* floor(log2 L) */
+  int64_t b = 4 * (int64_t)h + ((L >> (h - 2)) & 3) - 4;
+  return (int32_t)(b < 78 ? b : 78);
+}
+
+/* Request-level dispatch and batching inside one slot (
+ * P:1147 "latency (e.g., p50/p95) and SLO violation rate"; D10):
+ *   requests arrive evenly over the slot: request j at tau_j = floor(j*T/r) us;
+ *   batch k holds requests [k*IBS, min((k+1)*IBS, r)) -- the slot model's ceil(r/IBS)
+ *     batches (step 5) -- and is ready when its last member arrives (no SLO/2 timeout:
+ *     SPEC S:513's early firing would change the batch count the capacity model fixes);
+ *   the first b batches (the slot's executed batches, step 8) run back to back, each for
+ *     e us: start = max(ready, previous completion), completion = start + e;
+ *   a served request's latency = its batch's completion - its arrival; requests of
+ *     batches >= b are unserved.                                                     */
+void dilu_ref_instance_latency(int64_t r, int64_t ibs, int64_t b, int64_t e, int64_t slo_us,
+                               int64_t T_us, int64_t* lat) {
+  const int64_t need = (r + ibs - 1) / ibs;
+  int64_t prev = 0;
+  for (int64_t k = 0; k < need; ++k) {
+    const int64_t j0 = k * ibs, j1 = (k + 1) * ibs < r ? (k + 1) * ibs : r;
+    if (k >= b) {                                 /* not executed in this slot */
+      lat[REF_LAT_UNSERVED] += j1 - j0;
+      lat[80] += j1 - j0;
+      continue;
+    }
+    const int64_t ready = (j1 - 1) * T_us / r;    /* the last member's arrival */
+    const int64_t start = ready > prev ? ready : prev;
+    const int64_t done = start + e;
+    for (int64_t j = j0; j < j1; ++j) {
+      const int64_t L = done - j * T_us / r;
+      lat[dilu_ref_lat_bucket(L)] += 1;
+      lat[81] += L;
+      if (L > slo_us) lat[80] += 1;
+    }
+    prev = done;
+  }
 }
 
 /* ------------------------------------------------ lazy horizontal scaling */
@@ -794,7 +841,11 @@ static void slot(RScen* s, int32_t t) {
     s->tally[T_REQ_TOTAL] += A;
     int32_t nw = 0;
     for (int32_t j = 0; j < Fs->nlive; ++j) nw += s->inst[Fs->live[j]].warm;
-    if (nw == 0) { s->tally[T_REQ_VIOLATED] += A; continue; }   /* Q17 */
+    if (nw == 0) {                                               /* Q17 */
+      s->tally[T_REQ_VIOLATED] += A;
+      if (c->flags & 8) { s->lat[REF_LAT_UNSERVED] += A; s->lat[80] += A; }
+      continue;
+    }
     int32_t rank = 0;
     for (int32_t j = 0; j < Fs->nlive; ++j) {
       RInst* I = &s->inst[Fs->live[j]];
@@ -883,6 +934,16 @@ static void slot(RScen* s, int32_t t) {
     for (int32_t k = 0; k < I->nst; ++k) {
       s->gpu[I->g[k]].exec += b * cst;
       s->tally[T_INF_EXEC] += b * cst;
+    }
+    if (c->flags & 8) {
+      /* a batch runs at the slowest stage's rate: e = max_k ceil(c_stage * T / a_k) us */
+      const int64_t T_us = 1000LL * c->slot_ms;
+      int64_t e = 0;
+      for (int32_t k = 0; k < I->nst; ++k) {
+        const int64_t ek = I->a[k] > 0 ? (cst * T_us + I->a[k] - 1) / I->a[k] : 0;
+        if (ek > e) e = ek;
+      }
+      dilu_ref_instance_latency(I->r, Fn->ibs, b, e, s->slo_us[I->func], T_us, s->lat);
     }
   }
   for (int32_t f = 0; f < F; ++f) {                      /* training jobs: barrel effect (Q22) */
@@ -1019,9 +1080,12 @@ int32_t dilu_ref_create(const ref_config* cfg, const ref_scenario* scen, const r
     sc->mode = scen ? scen[i].mode : M_DILU;
     /* quota transforms of the baselines: MPS-l and FaST-GS+ run at the
      * limit quota, MPS-r at the request quota -- both without vertical scaling */
+    sc->slo_us = (int64_t*)xcalloc((size_t)cfg->max_funcs, sizeof(int64_t));
     for (int32_t f = 0; f < cfg->max_funcs; ++f) {
       ref_func* F = &s->funcs[(size_t)i * cfg->max_funcs + f];
       if (F->kind == K_UNUSED) continue;
+      /* SLO = 2 * t_exec at the profiled request (P:634 footnote, R4): c_b = req * SLO/2 */
+      if (is_inf(F->kind)) sc->slo_us[f] = 2000LL * F->work_per_batch / F->req_pm;
       if (sc->mode == M_STATIC_LIMIT || sc->mode == M_EAGER) F->req_pm = F->lim_pm;
       if (sc->mode == M_STATIC_REQUEST) F->lim_pm = F->req_pm;
     }
@@ -1040,7 +1104,7 @@ void dilu_ref_destroy(ref_sim* s) {
   for (int32_t i = 0; i < s->S; ++i) {
     RScen* sc = &s->sc[i];
     for (int32_t f = 0; f < s->cfg.max_funcs; ++f) { free(sc->fs[f].ring); free(sc->fs[f].live); }
-    free(sc->fs); free(sc->gpu); free(sc->inst); free(sc->q);
+    free(sc->fs); free(sc->gpu); free(sc->inst); free(sc->q); free(sc->slo_us);
   }
   free(s->sc); free(s->funcs); free(s->patterns); free(s);
 }
@@ -1140,6 +1204,19 @@ int32_t dilu_ref_metrics(ref_sim* s, int64_t* per_scenario, int64_t* sum) {
       acc[k] = (int64_t)((uint64_t)acc[k] + (uint64_t)s->sc[i].tally[k]);
     }
   }
+  if (sum) memcpy(sum, acc, sizeof acc);
+  return s->status;
+}
+
+int32_t dilu_ref_latency(ref_sim* s, int64_t* per_scenario, int64_t* sum) {
+  if (!s) return REF_E_USAGE;
+  int64_t acc[REF_NLAT];
+  memset(acc, 0, sizeof acc);
+  for (int32_t i = 0; i < s->S; ++i)
+    for (int32_t k = 0; k < REF_NLAT; ++k) {
+      if (per_scenario) per_scenario[(int64_t)i * REF_NLAT + k] = s->sc[i].lat[k];
+      acc[k] += s->sc[i].lat[k];
+    }
   if (sum) memcpy(sum, acc, sizeof acc);
   return s->status;
 }

@@ -40,7 +40,7 @@ typedef struct {
   int32_t n_scenarios, gpus_per_scenario, max_funcs, max_instances;
   int32_t q_pm, mem_mib, omega_pm, gamma_pm, alpha_w, beta_w, slot_ms;
   int32_t window_s, phi_out, phi_in, min_instances, max_residents, max_llm_stages;
-  int32_t n_patterns, pattern_len, flags;  /* bit0 LLM split, bit1 invariants, bit2 Alg.2 5 ms */
+  int32_t n_patterns, pattern_len, flags;  /* bit0 LLM split, bit1 invariants, bit2 Alg.2 5 ms, bit3 latency */
 } ref_config;
 
 /* mode: 0 Dilu, 1 Exclusive, 2 StaticLimit (MPS-l), 3 StaticRequest (MPS-r),
@@ -72,6 +72,24 @@ int32_t dilu_ref_slot_detail(ref_sim* s, int32_t scenario, int32_t id_cap, int64
                              int32_t* r, int64_t* exec);
 const char* dilu_ref_last_error(const ref_sim* s);
 void dilu_ref_destroy(ref_sim* s);
+
+/* ---- request-level latency (cfg.flags bit3) ----
+ * Per scenario a latency vector of REF_NLAT int64: [0, 79) log-spaced histogram of
+ * request latencies in microseconds (bucket of L: L < 4 -> L; else 4*h + next two
+ * bits - 4, h = floor(log2 L), capped at 78), [79] requests never served in their slot
+ * (no warm instance, or beyond the executed batches), [80] latency-SLO violations
+ * (latency > SLO, plus every unserved request), [81] sum of served latencies
+ * (us).  Readings DESIGN.md D10. */
+#define REF_NLAT 82
+#define REF_LAT_UNSERVED 79
+int32_t dilu_ref_latency(ref_sim* s, int64_t* per_scenario /* [S][82] or NULL */,
+                         int64_t* sum /* [82] */);
+int32_t dilu_ref_lat_bucket(int64_t L);
+/* one instance-slot: r requests arriving at floor(j*T/r), ceil(r/IBS) batches of which
+ * the first b execute back to back, each taking e us from max(its last member's
+ * arrival, the previous completion); adds into lat[REF_NLAT]. */
+void dilu_ref_instance_latency(int64_t r, int64_t ibs, int64_t b, int64_t e, int64_t slo_us,
+                               int64_t T_us, int64_t* lat);
 
 /* ---- literal Algorithm 2 at 5 ms periods (cfg.flags bit2) ----
  * Alg.2 IssueToken run per GPU every period ("periodically
