@@ -84,7 +84,8 @@ typedef struct {
   int32_t n_patterns, pattern_len;
   int32_t flags;              /* bit0: LLM worst-fit split enabled; bit2: literal Alg.2 at */
                               /* 5 ms periods (D8) instead of   */
-                              /* the slot-level grant; needs slot_ms % 5 == 0 (bit1 unused)  */
+                              /* the slot-level grant; needs slot_ms % 5 == 0; bit3: request- */
+                              /* level latency (dilu_latency, D10); bit1 unused               */
 } dilu_config;
 
 /* Per-scenario parameters (the C4 sweep varies gamma per scenario). */
@@ -175,6 +176,17 @@ dilu_status dilu_snapshot(dilu_sim* s, int32_t id_cap, int32_t* d_gpu, int32_t* 
  * in a -DDILU_PHASE_TIMING build).  Host or device pointers.
  * Synchronises the stream. */
 dilu_status dilu_kernel_stats(dilu_sim* s, int64_t* per_scenario, int64_t* sum);
+
+/* Request-level latency (cfg.flags bit3; "latency (e.g.,
+ * p50/p95) and SLO violation rate"; D10).  Per scenario DILU_NLAT int64:
+ * [0, 79) request-latency histogram in microseconds, 4 log buckets per octave (L < 4 ->
+ * bucket L, else 4*floor(log2 L) + next two bits - 4, capped at 78); [79] requests not
+ * served in their slot; [80] latency-SLO violations (latency > SLO = 2 * t_exec at the
+ * profiled request, plus every unserved request); [81] sum of served latencies.
+ * per_scenario [S][DILU_NLAT] and/or sum [DILU_NLAT], host or device pointers; syncs
+ * the stream.  DILU_E_USAGE if the handle was created without bit3. */
+#define DILU_NLAT 82
+dilu_status dilu_latency(dilu_sim* s, int64_t* per_scenario, int64_t* sum);
 
 /* Current slot (number of slots simulated so far). */
 int32_t dilu_current_slot(const dilu_sim* s);

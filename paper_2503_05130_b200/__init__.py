@@ -60,6 +60,8 @@ def lib():
         L.dilu_last_error.argtypes = [vp]
         L.dilu_sim_destroy.restype = None
         L.dilu_sim_destroy.argtypes = [vp]
+        L.dilu_latency.restype = i32
+        L.dilu_latency.argtypes = [vp, vp, vp]
         L.dilu_profile.restype = i32
         L.dilu_profile.argtypes = [vp, i32, vp, vp]
         _lib = L
@@ -69,7 +71,7 @@ def lib():
 EXPORTED = ["dilu_workspace_bytes", "dilu_sim_create", "dilu_sim_reset", "dilu_place_batch",
             "dilu_scale_step", "dilu_metrics", "dilu_snapshot", "dilu_kernel_stats",
             "dilu_current_slot",
-            "dilu_last_error", "dilu_sim_destroy", "dilu_profile"]
+            "dilu_last_error", "dilu_sim_destroy", "dilu_profile", "dilu_latency"]
 
 
 def _i32(a) -> np.ndarray:
@@ -172,6 +174,16 @@ class DiluSim:
         tot = np.zeros(24, dtype=np.int64)
         self._check(lib().dilu_kernel_stats(self.h, None, tot.ctypes.data))
         return dict(zip(self.STAT_NAMES, tot.tolist()))
+
+    NLAT = 82
+
+    def latency(self):
+        """Request-level latency vectors (dilu_latency; cfg.flags bit3): (per-scenario
+        [S][82] int64 numpy, sum [82])."""
+        per = np.zeros((self.S, self.NLAT), dtype=np.int64)
+        tot = np.zeros(self.NLAT, dtype=np.int64)
+        self._check(lib().dilu_latency(self.h, per.ctypes.data, tot.ctypes.data))
+        return per, tot
 
     @property
     def slot(self) -> int:

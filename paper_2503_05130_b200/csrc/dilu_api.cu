@@ -48,7 +48,7 @@ constexpr size_t ALIGN = 256;
 inline size_t up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
 
 struct Carve {
-  size_t funcs, pat, scen, state, ring, tally, stats, gscr, sum, total;
+  size_t funcs, pat, scen, state, ring, tally, stats, gscr, lat, sum, total;
 };
 
 bool check_cfg(const dilu_config* c, char* msg, size_t n) {
@@ -132,7 +132,7 @@ int choose_engine(const dilu_config* c) {
     if (!strcmp(v, "cta")) e = 0;
     if (!strcmp(v, "cluster")) e = 2;
     if (!strcmp(v, "lanes") && c->gpus_per_scenario <= 256 && c->max_funcs <= 4096 &&
-        c->max_instances <= 8192 && !(c->flags & 4))     // lanes: no literal Alg.2
+        c->max_instances <= 8192 && !(c->flags & 12))    // lanes: no Alg.2, no latency
       e = 1;
   }
   return e;
@@ -164,18 +164,21 @@ typedef void (*RunFn)(Params, int32_t*, int32_t, int32_t, int32_t, const int32_t
 typedef void (*ClusterFn)(Params, int32_t, int32_t, int32_t, const int32_t*, const int32_t*,
                           int32_t*, int32_t*);
 int variant_of(const dilu_config* c, const Layout& L) {
-  return (L.B > 1 ? 1 : 0) | ((c->flags & 4) ? 2 : 0);
+  return (L.B > 1 ? 1 : 0) | ((c->flags & 4) ? 2 : 0) | ((c->flags & 8) ? 4 : 0);
 }
 RunFn run_fn(bool smem, int var) {
-  static const RunFn tab[2][4] = {
-      {k_run<false, 0>, k_run<false, 1>, k_run<false, 2>, k_run<false, 3>},
-      {k_run<true, 0>, k_run<true, 1>, k_run<true, 2>, k_run<true, 3>}};
-  return tab[smem ? 1 : 0][var & 3];
+  static const RunFn tab[2][8] = {
+      {k_run<false, 0>, k_run<false, 1>, k_run<false, 2>, k_run<false, 3>,
+       k_run<false, 4>, k_run<false, 5>, k_run<false, 6>, k_run<false, 7>},
+      {k_run<true, 0>, k_run<true, 1>, k_run<true, 2>, k_run<true, 3>,
+       k_run<true, 4>, k_run<true, 5>, k_run<true, 6>, k_run<true, 7>}};
+  return tab[smem ? 1 : 0][var & 7];
 }
 ClusterFn cluster_fn(int var) {
-  static const ClusterFn tab[4] = {k_run_cluster<0>, k_run_cluster<1>, k_run_cluster<2>,
-                                   k_run_cluster<3>};
-  return tab[var & 3];
+  static const ClusterFn tab[8] = {k_run_cluster<0>, k_run_cluster<1>, k_run_cluster<2>,
+                                   k_run_cluster<3>, k_run_cluster<4>, k_run_cluster<5>,
+                                   k_run_cluster<6>, k_run_cluster<7>};
+  return tab[var & 7];
 }
 
 Carve carve(const dilu_config* c, const Layout& L) {
@@ -199,6 +202,7 @@ Carve carve(const dilu_config* c, const Layout& L) {
   k.tally = o; o = up(o + S * NT * 8);
   k.stats = o; o = up(o + S * NSTAT * 8);
   k.gscr = o; o = up(o + S * GSCR * 8);
+  k.lat = o; o = up(o + ((c->flags & 8) ? S * NLAT * 8 : 0));
   k.sum = o; o = up(o + (NT + 2) * 8);
   k.total = o;
   return k;
@@ -278,7 +282,8 @@ size_t dilu_workspace_bytes(const dilu_config* cfg) {
   char msg[256];
   if (!check_cfg(cfg, msg, sizeof msg)) return 0;
   const Layout L = make_layout(cfg->gpus_per_scenario, cfg->max_funcs, cfg->max_instances,
-                               cfg->window_s, choose_batch(cfg), (cfg->flags & 4) != 0);
+                               cfg->window_s, choose_batch(cfg), (cfg->flags & 4) != 0,
+                               (cfg->flags & 8) != 0);
   return carve(cfg, L).total;
 }
 
@@ -298,7 +303,7 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   s->cfg = *cfg;
   s->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   s->L = make_layout(cfg->gpus_per_scenario, cfg->max_funcs, cfg->max_instances, cfg->window_s,
-                     choose_batch(cfg), (cfg->flags & 4) != 0);
+                     choose_batch(cfg), (cfg->flags & 4) != 0, (cfg->flags & 8) != 0);
   const Carve k = carve(cfg, s->L);
   if (!d_workspace || ws_bytes < k.total || (reinterpret_cast<uintptr_t>(d_workspace) % ALIGN)) {
     fprintf(stderr, "dilu_sim_create: workspace needs %zu bytes, 256-byte aligned (got %zu)\n",
@@ -347,6 +352,7 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   P.tally = reinterpret_cast<int64_t*>(s->ws + k.tally);
   P.stats = reinterpret_cast<int64_t*>(s->ws + k.stats);
   P.gscratch = reinterpret_cast<unsigned long long*>(s->ws + k.gscr);
+  P.lat = (cfg->flags & 8) ? reinterpret_cast<int64_t*>(s->ws + k.lat) : nullptr;
   P.L = s->L;
   P.S = cfg->n_scenarios; P.G = cfg->gpus_per_scenario; P.F = cfg->max_funcs;
   P.I = cfg->max_instances; P.W = cfg->window_s; P.M = cfg->mem_mib; P.Q = cfg->q_pm;
@@ -561,6 +567,26 @@ dilu_status dilu_kernel_stats(dilu_sim* s, int64_t* per_scenario, int64_t* sum) 
     for (size_t i = 0; i < n; ++i) acc[i % NSTAT] += h[i];
     if (per_scenario) rc = cuda_check(s, cudaMemcpy(per_scenario, h, n * 8, cudaMemcpyDefault), "stats out");
     if (!rc && sum) rc = cuda_check(s, cudaMemcpy(sum, acc, sizeof acc, cudaMemcpyDefault), "stats sum");
+  }
+  delete[] h;
+  return rc;
+}
+
+dilu_status dilu_latency(dilu_sim* s, int64_t* per_scenario, int64_t* sum) {
+  if (!s) return DILU_E_USAGE;
+  if (s->status == DILU_E_CUDA) return DILU_E_STATE;
+  if (!(s->cfg.flags & 8)) return fail(s, DILU_E_USAGE, "latency: cfg.flags bit3 not set");
+  const size_t n = (size_t)s->cfg.n_scenarios * NLAT;
+  int64_t* h = new (std::nothrow) int64_t[n];
+  if (!h) return fail(s, DILU_E_USAGE, "out of host memory");
+  dilu_status rc = cuda_check(s, cudaMemcpyAsync(h, s->P.lat, n * 8, cudaMemcpyDeviceToHost, s->stream),
+                              "copy latency");
+  if (!rc) rc = cuda_check(s, cudaStreamSynchronize(s->stream), "latency sync");
+  if (!rc) {
+    int64_t acc[NLAT] = {0};
+    for (size_t i = 0; i < n; ++i) acc[i % NLAT] += h[i];
+    if (per_scenario) rc = cuda_check(s, cudaMemcpy(per_scenario, h, n * 8, cudaMemcpyDefault), "latency out");
+    if (!rc && sum) rc = cuda_check(s, cudaMemcpy(sum, acc, sizeof acc, cudaMemcpyDefault), "latency sum");
   }
   delete[] h;
   return rc;

@@ -35,6 +35,7 @@ struct Params {
   int64_t* tally;            // [S][NT]
   int64_t* stats;            // [S][NSTAT] kernel statistics
   unsigned long long* gscratch;  // [S][GSCR] cluster-collective scratch
+  int64_t* lat;              // [S][NLAT] request-level latency (cfg.flags bit3), else null
   Layout L;
   int32_t S, G, F, I, W, M, Q, aw, bw, slot_ms, SPS, phi_out, phi_in, min_inst, max_stages,
       flags, Tp;
@@ -76,6 +77,7 @@ struct Red {                 // reduction scratch (static shared)
   unsigned long long u64[2][32];
   int32_t i32[2][33];
   int32_t flag[2];           // [0] next queue entry / scenario counter, [1] queue length
+  unsigned long long lat[NLAT];   // request-level latency of this call (cfg.flags bit3)
   int32_t members[64];       // gang member slots of the request being placed
   Acc0 z;
 };
@@ -162,6 +164,7 @@ struct Scn {
   int32_t* flag;             // group-visible broadcast word
   Acc0* z;                   // leader tallies (shared)
   const int32_t* frow;       // this scenario's input function rows [F][16]
+  unsigned long long* lat;   // request-level latency accumulator (shared, [NLAT])
   int32_t scn_id, om, ga, mode;   // mode: baseline (0 Dilu, 1 Exclusive, 2 MPS-l, 3 MPS-r, 4 eager)
 };
 enum : int32_t { M_DILU = 0, M_EXCLUSIVE = 1, M_STATIC_LIMIT = 2, M_STATIC_REQUEST = 3, M_EAGER = 4 };
@@ -686,12 +689,74 @@ __device__ void rebuild_layout(Scn& c) {
   c.g.sync();
 }
 
+// ---- request-level latency (cfg.flags bit3; D10) ----------
+__device__ __forceinline__ int lat_bucket(long long L) {   // 4 log buckets per octave (us)
+  if (L < 4) return L < 0 ? 0 : (int)L;
+  const int h = 63 - __clzll(L);
+  const int b = 4 * h + (int)((L >> (h - 2)) & 3) - 4;
+  return b < 78 ? b : 78;
+}
+
+// One instance-slot: r requests arriving at floor(j*T/r) us, ceil(r/IBS) batches ready at
+// their last arrival, the first b running back to back for e us each; per-request
+// latencies go to the shared histogram (runs of equal buckets flushed once), unserved
+// requests to bucket LAT_UNSERVED.  Arrival times advance by quotient/remainder steps, so
+// only one division per batch remains.
+__device__ void lat_instance(unsigned long long* lat, int32_t r, int32_t ibs, int32_t b, long long e,
+                             int32_t slo, long long T) {
+  if (r <= 0) return;
+  const int32_t served = (long long)b * ibs < r ? b * ibs : r;
+  const long long q0 = T / r, r0 = T % r;
+  long long sum = 0, viol = 0, tq = 0, tr = 0, prev = 0;   // tau_j = tq (+ tr/r)
+  int cur = -1;
+  unsigned long long cnt = 0;
+  for (int32_t j0 = 0; j0 < served; j0 += ibs) {
+    const int32_t j1 = j0 + ibs < r ? j0 + ibs : r;
+    const long long ready = (long long)(j1 - 1) * T / r;
+    const long long done = (ready > prev ? ready : prev) + e;
+    for (int32_t j = j0; j < j1; ++j) {
+      const long long L = done - tq;
+      const int bk = lat_bucket(L);
+      if (bk != cur) {
+        if (cnt) atomicAdd(&lat[cur], cnt);
+        cur = bk;
+        cnt = 0;
+      }
+      ++cnt;
+      sum += L;
+      viol += L > slo;
+      tq += q0;
+      tr += r0;
+      if (tr >= r) { tr -= r; ++tq; }
+    }
+    prev = done;
+  }
+  if (cnt) atomicAdd(&lat[cur], cnt);
+  const int32_t uns = r - served;
+  if (uns) atomicAdd(&lat[LAT_UNSERVED], (unsigned long long)uns);
+  viol += uns;
+  if (viol) atomicAdd(&lat[LAT_VIOL], (unsigned long long)viol);
+  if (sum) atomicAdd(&lat[LAT_SUM], (unsigned long long)sum);
+}
+
+__device__ __forceinline__ void lat_unserved(unsigned long long* lat, int32_t A) {
+  if (A > 0) { atomicAdd(&lat[LAT_UNSERVED], (unsigned long long)A); atomicAdd(&lat[LAT_VIOL], (unsigned long long)A); }
+}
+
+// batch time of one stage: ceil(c_stage * T / a) us (<= T whenever a batch runs)
+__device__ __forceinline__ int32_t lat_e(int32_t cst, int32_t a, long long T) {
+  if (a <= 0) return 0;
+  const long long e = ((long long)cst * T + a - 1) / a;
+  return e < 0x7fffffffLL ? (int32_t)e : 0x7fffffff;
+}
+
 // ---- per-slot phases ------------------------------------------------------------------
 
 
 // P0: arrivals and even dispatch over warm instances (Q16, Q17).
 // A_f(t) = (pat[p_f][(t + phase_f) mod T_pat] * scale_f) >> 10; the pattern index is
 // advanced incrementally (set at registration), so no modulo runs per slot.
+template <bool LAT>
 __device__ void phase0(Scn& c, int32_t t, Acc& acc, int32_t pf_f, long long pf_x) {
   View& v = c.v;
   const Params& P = *c.P;
@@ -723,7 +788,11 @@ __device__ void phase0(Scn& c, int32_t t, Acc& acc, int32_t pf_f, long long pf_x
     int32_t nw = 0;
     for (int32_t s = lh[f]; s >= 0; s = nxt[s])
       nw += (st_of(meta[s]) == ST_PLACED && ready[s] <= t);
-    if (nw == 0) { acc.rvio += A; continue; }
+    if (nw == 0) {
+      acc.rvio += A;
+      if (LAT) lat_unserved(c.lat, A);
+      continue;
+    }
     const int32_t q = A / nw, rem = A - q * nw;
     int32_t rank = 0;
     for (int32_t s = lh[f]; s >= 0; s = nxt[s]) {
@@ -736,6 +805,7 @@ __device__ void phase0(Scn& c, int32_t t, Acc& acc, int32_t pf_f, long long pf_x
 }
 
 // P1: vertical token allocation per GPU row (Q13, Q14)
+template <bool LAT>
 __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
   View& v = c.v;
   const Params& P = *c.P;
@@ -829,8 +899,10 @@ __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
           const long long e = (long long)b * cst;
           acc.iexe += e;
           acc.etot += e;
+          if (LAT) lat_instance(c.lat, rr, ibs, b, lat_e(cst, a, T), v.fSlo[f], T);
         } else {
           atomicMin(&bmin[s], b);
+          if (LAT) atomicMax(&v.iEmax[par * P.I + s], lat_e(cst, a, T));
         }
       }
     }
@@ -839,6 +911,7 @@ __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
 
 // P2: cross-row minima -- training gang (Q22) and LLM pipeline stages (Q11); only the
 // training and LLM functions (static list fDefL) are visited.
+template <bool LAT>
 __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
   View& v = c.v;
   const Params& P = *c.P;
@@ -889,6 +962,11 @@ __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
         const long long e = (long long)nst * b * cst;
         acc.iexe += e;
         acc.etot += e;
+        if (LAT) {
+          int32_t* em = &v.iEmax[par * P.I + s];
+          lat_instance(c.lat, rr, ibs, b, *em, v.fSlo[f], (long long)P.T_slot);
+          *em = 0;
+        }
       }
     }
   }
@@ -904,6 +982,7 @@ __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
 // integer operations), so results are bit-identical; only the hash summation order moves
 // (it is a mod-2^64 sum, order-free by construction, R8).
 
+template <bool LAT>
 __device__ void phase0_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   View& v = c.v;
   const Params& P = *c.P;
@@ -945,7 +1024,11 @@ __device__ void phase0_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
         nw = 0;
         for (int32_t s = s0; s >= 0; s = nxt[s]) nw += (st_of(meta[s]) == ST_PLACED && ready[s] <= tu);
       }
-      if (nw == 0) { acc.rvio += A; continue; }
+      if (nw == 0) {
+        acc.rvio += A;
+        if (LAT) lat_unserved(c.lat, A);
+        continue;
+      }
       const int32_t q = A / nw, rem = A - q * nw;
       int32_t rank = 0;
       int32_t* __restrict__ ru = rb + (size_t)u * I;
@@ -961,6 +1044,7 @@ __device__ void phase0_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   }
 }
 
+template <bool LAT>
 __device__ void phase1_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   View& v = c.v;
   const Params& P = *c.P;
@@ -1052,8 +1136,10 @@ __device__ void phase1_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
             const long long e = (long long)b * cst;
             acc.iexe += e;
             acc.etot += e;
+            if (LAT) lat_instance(c.lat, rr, ibs, b, lat_e(cst, a, T), v.fSlo[f], T);
           } else {
             atomicMin(&v.bB[(size_t)u * I + s], b);
+            if (LAT) atomicMax(&v.eB[(size_t)u * I + s], lat_e(cst, a, T));
           }
         }
       }
@@ -1061,6 +1147,7 @@ __device__ void phase1_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   }
 }
 
+template <bool LAT>
 __device__ void phase2_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   View& v = c.v;
   const Params& P = *c.P;
@@ -1111,6 +1198,11 @@ __device__ void phase2_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
           const long long e = (long long)nst * b * cst;
           acc.iexe += e;
           acc.etot += e;
+          if (LAT) {
+            int32_t* em = &v.eB[(size_t)u * I + s];
+            lat_instance(c.lat, rr, ibs, b, *em, v.fSlo[f], (long long)P.T_slot);
+            *em = 0;
+          }
         }
       }
     }
@@ -1130,9 +1222,10 @@ __device__ __forceinline__ int32_t a2_grow(int32_t r_last) {   // ceil(max(R_las
   return (int32_t)((r * 5 + 3) / 4);
 }
 
+template <bool LAT>
 __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* rbase, size_t rstride,
                             int32_t* bminb, size_t bstride, int32_t* gangb, size_t gstride,
-                            Acc& acc) {
+                            int32_t* emaxb, Acc& acc) {
   View& v = c.v;
   const Params& P = *c.P;
   const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
@@ -1318,8 +1411,11 @@ __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* rbase, 
             const long long ee = (long long)b * cst;
             acc.iexe += ee;
             acc.etot += ee;
+            if (LAT) lat_instance(c.lat, rr, ibs, b, lat_e(cst, a, (long long)P.T_slot), v.fSlo[f],
+                                  (long long)P.T_slot);
           } else {
             atomicMin(&bminb[(size_t)u * bstride + s], b);
+            if (LAT) atomicMax(&emaxb[(size_t)u * bstride + s], lat_e(cst, a, (long long)P.T_slot));
           }
         }
       }
@@ -1528,6 +1624,9 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
   acc.z = &red.z;
   c.z = &red.z;
   if (threadIdx.x == 0) red.z = Acc0{};
+  c.lat = red.lat;
+  if (VAR & 4)
+    for (int k = threadIdx.x; k < NLAT; k += blockDim.x) red.lat[k] = 0;
   int ph = 0;
   View& v = c.v;
   __syncthreads();
@@ -1559,6 +1658,7 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
     for (int32_t t = t0; t < t0 + n_slots; ++t) {
       constexpr bool fused = (VAR & 1) != 0;
       constexpr bool alg2 = (VAR & 2) != 0;
+      constexpr bool lat = (VAR & 4) != 0;
 #ifdef DILU_PHASE_TIMING
       long long tk0 = clock64(), tk1;
 #define TICK(slot) do { tk1 = clock64(); if (c.g.leader()) acc.z->st[8 + (slot)] += tk1 - tk0; tk0 = tk1; } while (0)
@@ -1599,7 +1699,7 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
         if (B > t0 + n_slots - t) B = t0 + n_slots - t;
         if (B > P.L.B) B = P.L.B;
         if (t % P.SPS != 0) c.g.sync();   // previous batch's P2 has read rB / bB
-        phase0_b(c, t, B, acc);
+        phase0_b<lat>(c, t, B, acc);
         if (c.g.leader()) {
           const long long na = v.h[H_NACT];
           acc.z->act += na * B;
@@ -1610,16 +1710,16 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
         }
         c.g.sync();
         TICK(3);
-        if (alg2) phase1_alg2(c, t, B, v.rB, P.I, v.bB, P.I, v.gB, P.F, acc);
-        else phase1_b(c, t, B, acc);
+        if (alg2) phase1_alg2<lat>(c, t, B, v.rB, P.I, v.bB, P.I, v.gB, P.F, v.eB, acc);
+        else phase1_b<lat>(c, t, B, acc);
         c.g.sync();
         TICK(4);
-        phase2_b(c, t, B, acc);
+        phase2_b<lat>(c, t, B, acc);
         TICK(5);
         t += B - 1;
         continue;
       }
-      phase0(c, t, acc, pf_f, pf_x);
+      phase0<lat>(c, t, acc, pf_f, pf_x);
       if (c.g.leader()) {
         const long long na = v.h[H_NACT];
         acc.z->act += na;
@@ -1632,13 +1732,14 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
       TICK(3);
       if (alg2) {
         const int par = t & 1;
-        phase1_alg2(c, t, 1, v.iR + par * P.I, 0, v.iBmin + par * P.I, 0, v.fGang + par * P.F, 0, acc);
+        phase1_alg2<lat>(c, t, 1, v.iR + par * P.I, 0, v.iBmin + par * P.I, 0, v.fGang + par * P.F, 0,
+                         v.iEmax + par * P.I, acc);
       } else {
-        phase1(c, t, acc);
+        phase1<lat>(c, t, acc);
       }
       c.g.sync();
       TICK(4);
-      phase2(c, t, acc);
+      phase2<lat>(c, t, acc);
       TICK(5);
 #undef TICK
     }
@@ -1684,6 +1785,15 @@ __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem,
         for (int k = 0; k < NSTAT; ++k) atomicAdd(ST + k, (unsigned long long)acc.z->st[k]);
       }
     }
+  }
+  if (VAR & 4) {                       // request-level latency of this call
+    __syncthreads();
+    unsigned long long* LT = reinterpret_cast<unsigned long long*>(P.lat) + (size_t)sc * NLAT;
+    for (int k = threadIdx.x; k < NLAT; k += blockDim.x)
+      if (red.lat[k]) {
+        if (K == 1) LT[k] += red.lat[k];
+        else atomicAdd(LT + k, red.lat[k]);
+      }
   }
   if (SMEM) {
     __syncthreads();
@@ -1789,6 +1899,17 @@ __global__ void k_init(Params P) {
   }
   if (P.flags & 4)
     for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) { v.aSt[g] = A2_NONE; v.aOw[g] = -1; v.aDt[g] = 0; }
+  if (P.flags & 8) {                   // request-level latency (D10)
+    for (int k = threadIdx.x; k < NLAT; k += blockDim.x) P.lat[(size_t)sc * NLAT + k] = 0;
+    for (int32_t f = threadIdx.x; f < P.F; f += blockDim.x) {
+      const int32_t* r = rows + (size_t)f * 16;
+      // SLO = 2 * t_exec at the profiled request (R4): c_b = req * SLO / 2
+      v.fSlo[f] = is_inf(r[0]) ? (int32_t)(2000LL * r[6] / r[3]) : 0;
+    }
+    for (size_t k = threadIdx.x; k < 2 * (size_t)P.I; k += blockDim.x) v.iEmax[k] = 0;
+    if (P.L.B > 1)
+      for (size_t k = threadIdx.x; k < (size_t)P.L.B * P.I; k += blockDim.x) v.eB[k] = 0;
+  }
   if (P.L.B > 1) {
     for (size_t k = threadIdx.x; k < (size_t)P.L.B * P.I; k += blockDim.x) v.bB[k] = BIG;
     for (size_t k = threadIdx.x; k < (size_t)P.L.B * P.F; k += blockDim.x) v.gB[k] = BIG;

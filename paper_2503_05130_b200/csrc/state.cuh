@@ -20,6 +20,8 @@ constexpr int NT = 17;     // tally vector length
 constexpr int32_t BIG = 0x7fffffff;
 constexpr int RLOG = 64;   // release log ring (GPU, epoch) for the placement retry skip
 constexpr int NSTAT = 24;  // kernel statistics per scenario (dilu_kernel_stats): 8 counters + 16 timers
+constexpr int NLAT = 82;   // request-level latency vector: 80 buckets, violations, latency sum
+constexpr int LAT_UNSERVED = 79, LAT_VIOL = 80, LAT_SUM = 81;
 
 enum : int32_t { K_UNUSED = -1, K_INF = 0, K_LLM = 1, K_TRAIN = 2 };
 enum : int32_t { ST_FREE = 0, ST_PEND = 1, ST_PLACED = 2 };
@@ -50,13 +52,14 @@ struct Layout {
   size_t qFunc, qFirst, qN, qFail, qSlot, iQ;
   size_t rB, bB, gB;       // per-batch-slot r, LLM stage minimum, training gang (B > 1 only)
   size_t aTc, aTm, aRl, aLe, aSt, aOw, aDt;   // literal Alg.2 state (cfg.flags bit2 only)
+  size_t fSlo, iEmax, eB;  // request-level latency (cfg.flags bit3 only)
   size_t hot_bytes, bytes;
 };
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B = 1,
-                          bool alg2 = false) {
+                          bool alg2 = false, bool lat = false) {
   Layout L;
   L.G = G; L.F = F; L.I = I; L.W = W; L.B = B;
   size_t o = 0;
@@ -103,6 +106,11 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B 
   const size_t ai = alg2 ? (size_t)I * MAXST : 0, ag = alg2 ? (size_t)G : 0;
   L.aTc = take(4 * ai); L.aTm = take(4 * ai); L.aRl = take(4 * ai); L.aLe = take(4 * ai);
   L.aSt = take(4 * ag); L.aOw = take(4 * ag); L.aDt = take(4 * ag);
+  // request-level latency (D10): per-function SLO (us), per split instance the
+  // slowest stage's batch time, per slot parity [2][I] or per batch slot [B][I]
+  L.fSlo = take(lat ? 4 * (size_t)F : 0);
+  L.iEmax = take(lat ? 4 * 2 * (size_t)I : 0);
+  L.eB = take(lat && B > 1 ? 4 * (size_t)B * I : 0);
   L.bytes = align16(o);
   return L;
 }
@@ -122,6 +130,7 @@ struct View {
   int32_t *qFunc, *qFirst, *qN, *qFail, *qSlot, *iQ;
   int32_t *rB, *bB, *gB;
   int32_t *aTc, *aTm, *aRl, *aLe, *aSt, *aOw, *aDt;
+  int32_t *fSlo, *iEmax, *eB;
   int32_t* ring;  // global [F][W]
 };
 
@@ -147,6 +156,7 @@ inline View make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
   P32(qFunc); P32(qFirst); P32(qN); P32(qFail); P32(qSlot); P32(iQ);
   P32(rB); P32(bB); P32(gB);
   P32(aTc); P32(aTm); P32(aRl); P32(aLe); P32(aSt); P32(aOw); P32(aDt);
+  P32(fSlo); P32(iEmax); P32(eB);
 #undef P32
   v.ring = nullptr;
   return v;

@@ -298,3 +298,48 @@ def test_alg2_fused_100ms(shape, monkeypatch):
     funcs[:, :, di.FI["cold_slots"]] += 3 * live
     wl = with_alg2(di.Workload("C5b", wl.cfg, wl.scen, funcs, wl.patterns, wl.n_slots))
     run_pair(wl, [1, 13, 186, 200], id_cap=16384)
+
+
+# ------------------------------------------- request-level latency (s8(f) #4, D10)
+
+def with_flags(wl, extra):
+    cfg = dict(wl.cfg, flags=wl.cfg["flags"] | extra)
+    return di.Workload(wl.name, cfg, wl.scen, wl.funcs, wl.patterns, wl.n_slots, wl.note)
+
+
+def latency_pair(wl, chunks, id_cap=None):
+    gs, rs, tot = run_pair(wl, chunks, id_cap=id_cap)
+    gl, gsum = gs.latency()
+    rl, rsum = rs.latency()
+    assert np.array_equal(gl, rl), f"latency differs at {np.argwhere(gl != rl)[:5].tolist()}"
+    assert gsum[:79].sum() == tot[T["req_served"]] and gsum[79] == tot[T["req_violated"]]
+    return gsum
+
+
+@pytest.mark.parametrize("seed", [0, 2])
+def test_latency_c2(seed):
+    lat = latency_pair(with_flags(di.c2(seed=seed, T=600), 8), [1, 299, 300], id_cap=4096)
+    assert lat[81] > 0
+
+
+@pytest.mark.parametrize("engine", ["cta", "cluster"])
+def test_latency_modes_c4_slice(engine, monkeypatch):
+    monkeypatch.setenv("DILU_ENGINE", engine)
+    wl = di.c4(n_scenarios=4096, T=300).subset(np.arange(7, 4096, 102))
+    latency_pair(with_flags(di.with_modes(wl, np.arange(wl.S) % 5), 8), [1, 299], id_cap=2048)
+
+
+def test_latency_llm_split_and_alg2():
+    wl = di.c4(n_scenarios=4096, T=240).subset(np.arange(0, 640, 61))
+    latency_pair(with_flags(wl, 8), [240])
+    latency_pair(with_flags(wl, 8 | 4), [240])
+
+
+@pytest.mark.parametrize("shape", ["cluster_b10", "cta_b10"])
+def test_latency_fused_100ms(shape, monkeypatch):
+    engine, _, b = shape.partition("_")
+    monkeypatch.setenv("DILU_ENGINE", engine)
+    monkeypatch.setenv("DILU_BATCH", b[1:])
+    wl = di.scaled("C5b", 512, 60, 120, 360, 100, 400, [53, 54], max_instances=8192)
+    latency_pair(with_flags(wl, 8), [1, 13, 386], id_cap=16384)
+    latency_pair(with_flags(wl, 8 | 4), [1, 13, 386], id_cap=16384)
