@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample scenarios (0: auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--latency", action="store_true",
+                    help="request-level latency (cfg.flags bit3, DESIGN.md D10): adds p50/p95 "
+                         "and the latency SVR to the line")
     ap.add_argument("--vertical", default="slot", choices=["slot", "alg2"],
                     help="slot: slot-level grant (default); alg2: literal Algorithm 2 at 5 ms "
                          "periods (cfg.flags bit2, DESIGN.md D8)")
@@ -69,13 +72,17 @@ def parse():
 
 
 def build_workload(name: str, rank: int, world: int, scaling: str, slots: int,
-                   vertical: str = "slot"):
+                   vertical: str = "slot", latency: bool = False):
+    import dilu_inputs as di
     wl, desc, n = _build_workload(name, rank, world, scaling, slots)
-    if vertical == "alg2":
-        import dilu_inputs as di
-        cfg = dict(wl.cfg, flags=wl.cfg["flags"] | 4)
+    extra = (4 if vertical == "alg2" else 0) | (8 if latency else 0)
+    if extra:
+        cfg = dict(wl.cfg, flags=wl.cfg["flags"] | extra)
         wl = di.Workload(wl.name, cfg, wl.scen, wl.funcs, wl.patterns, wl.n_slots, wl.note)
+    if vertical == "alg2":
         desc += "; literal Alg.2, %d x 5 ms periods per slot" % (wl.cfg["slot_ms"] // 5)
+    if latency:
+        desc += "; request-level latency"
     return wl, desc, n
 
 
@@ -176,7 +183,8 @@ def run_reference(args):
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     if rank != 0:
         return
-    wl, desc, n_slots = build_workload(args.workload, 0, 1, args.scaling, args.slots, args.vertical)
+    wl, desc, n_slots = build_workload(args.workload, 0, 1, args.scaling, args.slots, args.vertical,
+                                       args.latency)
     cores = len(os.sched_getaffinity(0))
     sample = args.cpu_sample or max(cores, min(wl.S, 2 * cores))
     vals = []
@@ -208,7 +216,7 @@ def run_dilu(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     wl, desc, n_slots = build_workload(args.workload, rank, world, args.scaling, args.slots,
-                                        args.vertical)
+                                        args.vertical, args.latency)
     sim = DiluSim.from_workload(wl, device=dev)
     stream = sim.stream
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -248,6 +256,13 @@ def run_dilu(args):
     D_all = int(tally[15].item())                        # all ranks (after the all-reduce)
     value = D_all * args.steps / (max_ms / 1000.0)
     stats = sim.kernel_stats()
+    lat_line = None
+    if args.latency:
+        from paper_2503_05130_b200 import latency_summary
+        _, lat = sim.latency()
+        lat_t = torch.from_numpy(lat).to(dev)
+        ddist.allreduce_tallies(lat_t)                  # int64 SUM over ranks
+        lat_line = latency_summary(lat_t.cpu().numpy())
 
     # roofline of the dominant kernel (k_run = the scale_step launch), algorithmic ops
     sps = 1000 // wl.cfg["slot_ms"]
@@ -308,7 +323,8 @@ def run_dilu(args):
             "config": {"workload": desc, "scenarios_per_gpu": wl.S, "gpus_per_scenario": wl.G,
                        "slots": n_slots, "slot_ms": wl.cfg["slot_ms"], "decisions_per_step": D_all,
                        "l2": "flushed between timed steps (256 MiB write)",
-                       "parallelism": f"scenario shards x{world}", "vertical": args.vertical},
+                       "parallelism": f"scenario shards x{world}", "vertical": args.vertical,
+                       "latency": bool(args.latency)},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": INT_PEAK_TOPS,
                          "unit": "Tops/s", "frac": achieved / INT_PEAK_TOPS, "traffic": traffic,
                          "kernel": "k_run (one launch per step)", "kernel_ms": 1000 * k_s,
@@ -320,6 +336,8 @@ def run_dilu(args):
             "clocks": clk.summary(),
             "kernel_stats_per_step": stats,
         }
+        if lat_line is not None:
+            line["latency"] = lat_line
         print(json.dumps(line), flush=True)
     ddist.barrier()
 

@@ -223,3 +223,35 @@ def dilu_profile(sessions, out=None, stream=None):
     if rc:
         raise DiluError(rc, "dilu_profile failed")
     return out
+
+
+def lat_bucket_bounds(b: int):
+    """[lo, hi) in microseconds of latency bucket b (D10), hi = inf for 79."""
+    if b >= 79:
+        return float("inf"), float("inf")
+    if b < 4:
+        return float(b), float(b + 1)
+    h, sub = (b + 4) // 4, (b + 4) % 4
+    lo = (1 << h) + sub * (1 << (h - 2))
+    return float(lo), float(lo + (1 << (h - 2)))
+
+
+def latency_summary(lat) -> dict:
+    """p50 / p95 / p99 (upper bucket bounds, ms), mean served latency and latency SVR
+    from a dilu_latency vector (reporting only: the histogram itself is the GPU's)."""
+    lat = np.asarray(lat, dtype=np.int64)
+    hist = lat[:80]
+    n = int(hist.sum())
+    served = int(hist[:79].sum())
+    out = {"requests": n, "served": served,
+           "latency_svr": float(lat[80]) / n if n else 0.0,
+           "mean_ms": float(lat[81]) / served / 1000.0 if served else None}
+    cum = np.cumsum(hist)
+    for q in (50, 95, 99):
+        if n == 0:
+            out[f"p{q}_ms"] = None
+            continue
+        b = int(np.searchsorted(cum, q / 100.0 * n, side="left"))
+        hi = lat_bucket_bounds(b)[1]
+        out[f"p{q}_ms"] = hi / 1000.0 if hi != float("inf") else None
+    return out

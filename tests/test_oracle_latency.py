@@ -84,3 +84,22 @@ def test_latency_under_alg2_and_modes():
         lper, lat = s.latency()
         assert (lper[:, :79].sum(1) == per[:, T["req_served"]]).all()
         assert (lper[:, 79] == per[:, T["req_violated"]]).all()
+
+
+def test_host_percentile_bounds_match_buckets():
+    """The host's bucket bounds (percentile reporting) contain every latency the oracle's
+    bucket function maps there; percentiles of a known histogram."""
+    from paper_2503_05130_b200 import lat_bucket_bounds, latency_summary
+    for L in list(range(0, 3000)) + [10 ** k + d for k in range(3, 9) for d in (-1, 0, 1)]:
+        lo, hi = lat_bucket_bounds(oracle.lat_bucket(L))
+        assert lo <= L < hi or oracle.lat_bucket(L) == 78
+    lat = np.zeros(82, np.int64)
+    lat[oracle.lat_bucket(1000)] = 50          # 50 requests at ~1 ms
+    lat[oracle.lat_bucket(20000)] = 45         # 45 at ~20 ms
+    lat[79] = 5                                # 5 unserved
+    lat[80] = 5
+    lat[81] = 50 * 1000 + 45 * 20000
+    s = latency_summary(lat)
+    assert s["p50_ms"] == lat_bucket_bounds(oracle.lat_bucket(1000))[1] / 1000
+    assert s["p95_ms"] == lat_bucket_bounds(oracle.lat_bucket(20000))[1] / 1000
+    assert s["p99_ms"] is None and s["latency_svr"] == 0.05
