@@ -17,6 +17,7 @@
 #include "sim_kernel.cuh"
 #include "sim_lanes.cuh"
 #include "profile.cuh"
+#include "variants.h"
 
 using namespace dilu;
 
@@ -158,27 +159,26 @@ int choose_parts() {
   return p;
 }
 
-// Kernel variant for a handle: bit0 fused sub-second batches, bit1 literal Alg.2 periods.
-typedef void (*RunFn)(Params, int32_t*, int32_t, int32_t, int32_t, const int32_t*, const int32_t*,
-                      int32_t*, int32_t*);
-typedef void (*ClusterFn)(Params, int32_t, int32_t, int32_t, const int32_t*, const int32_t*,
-                          int32_t*, int32_t*);
+// Kernel variant for a handle: bit0 fused sub-second batches, bit1 literal Alg.2 periods,
+// bit2 request-level latency (instantiated in run_variants.cu, see variants.h).
 int variant_of(const dilu_config* c, const Layout& L) {
   return (L.B > 1 ? 1 : 0) | ((c->flags & 4) ? 2 : 0) | ((c->flags & 8) ? 4 : 0);
 }
 RunFn run_fn(bool smem, int var) {
-  static const RunFn tab[2][8] = {
-      {k_run<false, 0>, k_run<false, 1>, k_run<false, 2>, k_run<false, 3>,
-       k_run<false, 4>, k_run<false, 5>, k_run<false, 6>, k_run<false, 7>},
-      {k_run<true, 0>, k_run<true, 1>, k_run<true, 2>, k_run<true, 3>,
-       k_run<true, 4>, k_run<true, 5>, k_run<true, 6>, k_run<true, 7>}};
-  return tab[smem ? 1 : 0][var & 7];
+  switch ((var & 7) >> 1) {
+    case 0: return run_fn_group0(smem, var);
+    case 1: return run_fn_group1(smem, var);
+    case 2: return run_fn_group2(smem, var);
+    default: return run_fn_group3(smem, var);
+  }
 }
 ClusterFn cluster_fn(int var) {
-  static const ClusterFn tab[8] = {k_run_cluster<0>, k_run_cluster<1>, k_run_cluster<2>,
-                                   k_run_cluster<3>, k_run_cluster<4>, k_run_cluster<5>,
-                                   k_run_cluster<6>, k_run_cluster<7>};
-  return tab[var & 7];
+  switch ((var & 7) >> 1) {
+    case 0: return cluster_fn_group0(var);
+    case 1: return cluster_fn_group1(var);
+    case 2: return cluster_fn_group2(var);
+    default: return cluster_fn_group3(var);
+  }
 }
 
 Carve carve(const dilu_config* c, const Layout& L) {

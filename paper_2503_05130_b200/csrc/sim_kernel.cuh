@@ -57,13 +57,13 @@ struct Acc {   // per-thread tallies
   Acc0* z;     // shared, written by thread 0 only
 };
 
-__device__ __forceinline__ uint64_t sm64(uint64_t z) {
+static __device__ __forceinline__ uint64_t sm64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
-__device__ __forceinline__ uint64_t mix5(uint32_t scn, uint32_t t, uint32_t i, uint32_t g,
+static __device__ __forceinline__ uint64_t mix5(uint32_t scn, uint32_t t, uint32_t i, uint32_t g,
                                          uint32_t a) {
   uint64_t h = sm64(scn);
   h = sm64(h ^ t);
@@ -83,7 +83,7 @@ struct Red {                 // reduction scratch (static shared)
 };
 
 // One-sync block min; double-buffered so back-to-back calls do not race.
-__device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v, Red& r,
+static __device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v, Red& r,
                                                             int& phase) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
@@ -105,7 +105,7 @@ __device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v
 }
 
 // One-sync block exclusive scan of int32; returns exclusive prefix, *total.
-__device__ __forceinline__ int32_t block_scan_i32(int32_t v, Red& r, int& phase,
+static __device__ __forceinline__ int32_t block_scan_i32(int32_t v, Red& r, int& phase,
                                                   int32_t* total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int32_t x = v;
@@ -134,7 +134,7 @@ __device__ __forceinline__ int32_t block_scan_i32(int32_t v, Red& r, int& phase,
 // ones followed by one hardware cluster barrier (release/acquire, which also makes the
 // other CTAs' global writes visible) over a small per-scenario global scratch.
 
-__device__ __forceinline__ void cluster_sync_all() {
+static __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
                ::: "memory");
 }
@@ -173,13 +173,13 @@ enum : int32_t { A2_NONE = 0, A2_EMERGENCY = 1, A2_RECOVERY = 2, A2_CONTENTION =
 constexpr int32_t A2_PERIOD_MS = 5, A2_MAX_TOKENS = 5000, A2_ETA_V = 300, A2_RW = 20;
 constexpr int32_t A2_NEVER = -(1 << 30);
 
-__device__ __forceinline__ int st_of(int32_t meta) { return meta & 3; }
-__device__ __forceinline__ int nst_of(int32_t meta) { return (meta >> 4) & 7; }
-__device__ __forceinline__ bool is_inf(int32_t k) { return k == K_INF || k == K_LLM; }
+static __device__ __forceinline__ int st_of(int32_t meta) { return meta & 3; }
+static __device__ __forceinline__ int nst_of(int32_t meta) { return (meta >> 4) & 7; }
+static __device__ __forceinline__ bool is_inf(int32_t k) { return k == K_INF || k == K_LLM; }
 
 // ---- group collectives (K = 1: CTA-level; K > 1: CTA-level then one cluster barrier) --
 
-__device__ unsigned long long g_min_u64(Scn& c, unsigned long long v, Red& red, int& ph) {
+static __device__ unsigned long long g_min_u64(Scn& c, unsigned long long v, Red& red, int& ph) {
   v = block_min_u64(v, red, ph);
   if (c.g.K == 1) return v;
   unsigned long long* buf = c.g.gu + (c.g.cph & 1) * 16;
@@ -190,7 +190,7 @@ __device__ unsigned long long g_min_u64(Scn& c, unsigned long long v, Red& red, 
   for (int k = 0; k < c.g.K; ++k) { const unsigned long long x = __ldcg(buf + k); m = x < m ? x : m; }
   return m;
 }
-__device__ int32_t g_sum_i32(Scn& c, int32_t cta_value) {   // cta_value uniform within the CTA
+static __device__ int32_t g_sum_i32(Scn& c, int32_t cta_value) {   // cta_value uniform within the CTA
   if (c.g.K == 1) return cta_value;
   int32_t* buf = c.g.gi + (c.g.cph & 1) * 16;
   if (threadIdx.x == 0) buf[c.g.crank] = cta_value;
@@ -200,9 +200,9 @@ __device__ int32_t g_sum_i32(Scn& c, int32_t cta_value) {   // cta_value uniform
   for (int k = 0; k < c.g.K; ++k) r += __ldcg(buf + k);
   return r;
 }
-__device__ bool g_any(Scn& c, bool p) { return g_sum_i32(c, __syncthreads_or(p)) != 0; }
-__device__ int32_t g_count(Scn& c, int p) { return g_sum_i32(c, __syncthreads_count(p)); }
-__device__ int32_t g_scan(Scn& c, int32_t v, Red& red, int& ph, int32_t* total) {
+static __device__ bool g_any(Scn& c, bool p) { return g_sum_i32(c, __syncthreads_or(p)) != 0; }
+static __device__ int32_t g_count(Scn& c, int p) { return g_sum_i32(c, __syncthreads_count(p)); }
+static __device__ int32_t g_scan(Scn& c, int32_t v, Red& red, int& ph, int32_t* total) {
   int32_t ctot;
   const int32_t pre = block_scan_i32(v, red, ph, &ctot);
   if (c.g.K == 1) { *total = ctot; return pre; }
@@ -222,12 +222,12 @@ __device__ int32_t g_scan(Scn& c, int32_t v, Red& red, int& ph, int32_t* total) 
 
 // ---- serial helpers (thread 0 only) ------------------------------------------------
 
-__device__ void list_append(View& v, int32_t f, int32_t s) {
+static __device__ void list_append(View& v, int32_t f, int32_t s) {
   v.iNext[s] = -1;
   if (v.fLt[f] < 0) v.fLh[f] = s; else v.iNext[v.fLt[f]] = s;
   v.fLt[f] = s;
 }
-__device__ void list_remove(View& v, int32_t f, int32_t s) {
+static __device__ void list_remove(View& v, int32_t f, int32_t s) {
   int32_t prev = -1, cur = v.fLh[f];
   while (cur >= 0 && cur != s) { prev = cur; cur = v.iNext[cur]; }
   if (cur < 0) return;
@@ -237,11 +237,11 @@ __device__ void list_remove(View& v, int32_t f, int32_t s) {
 }
 
 // resident order key: (prio, id) -- SLO-sensitive first (Alg.2)
-__device__ __forceinline__ long long res_key(const View& v, int32_t s) {
+static __device__ __forceinline__ long long res_key(const View& v, int32_t s) {
   return ((long long)v.fPrio[v.iFunc[s]] << 32) | (uint32_t)v.iId[s];
 }
 
-__device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
+static __device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
   View& v = c.v;
   const int32_t f = v.iFunc[s];
   if (v.gN[g] == 0) v.h[H_NACT] += 1;
@@ -270,7 +270,7 @@ __device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
   v.h[H_DIRTY] = 1;
 }
 
-__device__ void release(Scn& c, int32_t s) {
+static __device__ void release(Scn& c, int32_t s) {
   View& v = c.v;
   const int32_t f = v.iFunc[s];
   const int32_t meta = v.iMeta[s];
@@ -306,13 +306,13 @@ __device__ void release(Scn& c, int32_t s) {
 #define TSTART do { } while (0)
 #define TSTOP(k) do { } while (0)
 #endif
-__device__ void terminate_impl(Scn& c, int32_t s);
-__device__ void terminate(Scn& c, int32_t s) {
+static __device__ void terminate_impl(Scn& c, int32_t s);
+static __device__ void terminate(Scn& c, int32_t s) {
   TSTART;
   terminate_impl(c, s);
   TSTOP(15);
 }
-__device__ void terminate_impl(Scn& c, int32_t s) {
+static __device__ void terminate_impl(Scn& c, int32_t s) {
   View& v = c.v;
   const int32_t f = v.iFunc[s];
   if (st_of(v.iMeta[s]) == ST_PLACED) {
@@ -334,7 +334,7 @@ __device__ void terminate_impl(Scn& c, int32_t s) {
   v.fstack[v.h[H_FSTOP]++] = s;
 }
 
-__device__ void compact_queue(View& v) {
+static __device__ void compact_queue(View& v) {
   const int32_t n = v.h[H_QLEN];
   int32_t k = 0;
   for (int32_t q = 0; q < n; ++q) {
@@ -350,14 +350,14 @@ __device__ void compact_queue(View& v) {
 }
 
 // enqueue one request of n new instances of f; returns first id or -1 on capacity error
-__device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n);
-__device__ int32_t enqueue(Scn& c, int32_t f, int32_t n) {
+static __device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n);
+static __device__ int32_t enqueue(Scn& c, int32_t f, int32_t n) {
   TSTART;
   const int32_t r = enqueue_impl(c, f, n);
   TSTOP(16);
   return r;
 }
-__device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
+static __device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
   View& v = c.v;
   if (v.h[H_FSTOP] < n) { v.h[H_ERR] = 6; return -1; }
   if (v.h[H_QLEN] == c.P->I) compact_queue(v);
@@ -382,7 +382,7 @@ __device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
   return first;
 }
 
-__device__ void register_func(View& v, int32_t f, int32_t t, int32_t Tp) {
+static __device__ void register_func(View& v, int32_t f, int32_t t, int32_t Tp) {
   if (v.fReg[f]) return;
   v.fReg[f] = 1;
   v.fNsamp[f] = 0; v.fAcc[f] = 0; v.fHead[f] = 0; v.fUp[f] = 0; v.fDown[f] = 0;
@@ -390,12 +390,12 @@ __device__ void register_func(View& v, int32_t f, int32_t t, int32_t Tp) {
   v.fPidx[f] = (int32_t)(((long long)t + v.fPhase[f]) % Tp);   // arrivals index for slot t
 }
 
-__device__ void kill_queue_entries_of(View& v, int32_t f) {
+static __device__ void kill_queue_entries_of(View& v, int32_t f) {
   const int32_t n = v.h[H_QLEN];
   for (int32_t q = 0; q < n; ++q) if (v.qN[q] > 0 && v.qFunc[q] == f) v.qN[q] = 0;
 }
 
-__device__ void kill_queue_entry_with_id(View& v, int32_t id) {
+static __device__ void kill_queue_entry_with_id(View& v, int32_t id) {
   const int32_t n = v.h[H_QLEN];
   for (int32_t q = 0; q < n; ++q)
     if (v.qN[q] > 0 && v.qFirst[q] <= id && id < v.qFirst[q] + v.qN[q]) { v.qN[q] = 0; return; }
@@ -405,7 +405,7 @@ __device__ void kill_queue_entry_with_id(View& v, int32_t id) {
 
 // Algorithm 1 for one instance s with Principle 2's LLM split before a new
 // GPU (Q11).  All threads call; thread 0 commits.  Returns a uniform success flag.
-__device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
+static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
   View& v = c.v;
   const Params& P = *c.P;
   const int32_t f = v.iFunc[s];
@@ -496,7 +496,7 @@ __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
 // Can GPU g, released after a request of f last failed, now change that outcome?
 // Non-LLM: g hosts one instance now (an emptied GPU always can).  LLM with split
 // enabled: g is also a split candidate (caps hold, some free memory).
-__device__ __forceinline__ bool could_help(const Scn& c, int32_t g, int32_t f) {
+static __device__ __forceinline__ bool could_help(const Scn& c, int32_t g, int32_t f) {
   const View& v = c.v;
   const Params& P = *c.P;
   const int32_t n = v.gN[g];
@@ -509,7 +509,7 @@ __device__ __forceinline__ bool could_help(const Scn& c, int32_t g, int32_t f) {
 // Could any GPU released after epoch fe now host a request of f?  Walks the release
 // log back to fe (usually 1-3 entries); falls back to scanning every GPU's last-release
 // epoch when the log no longer covers fe.
-__device__ bool hope_after(const Scn& c, int32_t fe, int32_t f) {
+static __device__ bool hope_after(const Scn& c, int32_t fe, int32_t f) {
   const View& v = c.v;
   const int32_t n = v.h[H_RLN];
   const int32_t lo = n > RLOG ? n - RLOG : 0;
@@ -529,7 +529,7 @@ __device__ bool hope_after(const Scn& c, int32_t fe, int32_t f) {
 // requests that fail again by the skip rule are counted and stamped with the current
 // epoch; returns the first entry that needs a real attempt, or qn.  Lane 0 is thread 0
 // (owner of the thread-0 tallies).
-__device__ int32_t next_attempt(Scn& c, int32_t q, int32_t qn, Acc& acc) {
+static __device__ int32_t next_attempt(Scn& c, int32_t q, int32_t qn, Acc& acc) {
   View& v = c.v;
   const int lane = threadIdx.x & 31;
   const int32_t ep = v.h[H_EPOCH];
@@ -574,7 +574,7 @@ __device__ int32_t next_attempt(Scn& c, int32_t q, int32_t qn, Acc& acc) {
 // Entered without a group barrier after B3 (the leader's serial event pass): only warp 0
 // (which contains the leader) reads the queue before the first barrier below, and it
 // broadcasts the queue length with the first attempt index.
-__device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
+static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
   View& v = c.v;
   int32_t qn = 0;
   bool removed = false;                 // leader only
@@ -651,11 +651,11 @@ __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
 
 // ---- B5: pack GPU rows into 32-lane warp chunks by width class (1..32 lanes) ----------
 
-__device__ __forceinline__ int width_class(int32_t n) {
+static __device__ __forceinline__ int width_class(int32_t n) {
   return n <= 1 ? 0 : 32 - __clz(n - 1);
 }
 
-__device__ void rebuild_layout(Scn& c) {
+static __device__ void rebuild_layout(Scn& c) {
   View& v = c.v;
   const Params& P = *c.P;
   if (c.g.crank == 0 && threadIdx.x < 6) { v.h[H_CCNT + threadIdx.x] = 0; v.h[H_CCNT2 + threadIdx.x] = 0; }
@@ -690,7 +690,7 @@ __device__ void rebuild_layout(Scn& c) {
 }
 
 // ---- request-level latency (cfg.flags bit3; D10) ----------
-__device__ __forceinline__ int lat_bucket(long long L) {   // 4 log buckets per octave (us)
+static __device__ __forceinline__ int lat_bucket(long long L) {   // 4 log buckets per octave (us)
   if (L < 4) return L < 0 ? 0 : (int)L;
   const int h = 63 - __clzll(L);
   const int b = 4 * h + (int)((L >> (h - 2)) & 3) - 4;
@@ -702,7 +702,7 @@ __device__ __forceinline__ int lat_bucket(long long L) {   // 4 log buckets per 
 // latencies go to the shared histogram (runs of equal buckets flushed once), unserved
 // requests to bucket LAT_UNSERVED.  Arrival times advance by quotient/remainder steps, so
 // only one division per batch remains.
-__device__ void lat_instance(unsigned long long* lat, int32_t r, int32_t ibs, int32_t b, long long e,
+static __device__ void lat_instance(unsigned long long* lat, int32_t r, int32_t ibs, int32_t b, long long e,
                              int32_t slo, long long T) {
   if (r <= 0) return;
   const int32_t served = (long long)b * ibs < r ? b * ibs : r;
@@ -739,12 +739,12 @@ __device__ void lat_instance(unsigned long long* lat, int32_t r, int32_t ibs, in
   if (sum) atomicAdd(&lat[LAT_SUM], (unsigned long long)sum);
 }
 
-__device__ __forceinline__ void lat_unserved(unsigned long long* lat, int32_t A) {
+static __device__ __forceinline__ void lat_unserved(unsigned long long* lat, int32_t A) {
   if (A > 0) { atomicAdd(&lat[LAT_UNSERVED], (unsigned long long)A); atomicAdd(&lat[LAT_VIOL], (unsigned long long)A); }
 }
 
 // batch time of one stage: ceil(c_stage * T / a) us (<= T whenever a batch runs)
-__device__ __forceinline__ int32_t lat_e(int32_t cst, int32_t a, long long T) {
+static __device__ __forceinline__ int32_t lat_e(int32_t cst, int32_t a, long long T) {
   if (a <= 0) return 0;
   const long long e = ((long long)cst * T + a - 1) / a;
   return e < 0x7fffffffLL ? (int32_t)e : 0x7fffffff;
@@ -757,7 +757,7 @@ __device__ __forceinline__ int32_t lat_e(int32_t cst, int32_t a, long long T) {
 // A_f(t) = (pat[p_f][(t + phase_f) mod T_pat] * scale_f) >> 10; the pattern index is
 // advanced incrementally (set at registration), so no modulo runs per slot.
 template <bool LAT>
-__device__ void phase0(Scn& c, int32_t t, Acc& acc, int32_t pf_f, long long pf_x) {
+static __device__ void phase0(Scn& c, int32_t t, Acc& acc, int32_t pf_f, long long pf_x) {
   View& v = c.v;
   const Params& P = *c.P;
   const int32_t* __restrict__ infl = v.fInfL;
@@ -806,7 +806,7 @@ __device__ void phase0(Scn& c, int32_t t, Acc& acc, int32_t pf_f, long long pf_x
 
 // P1: vertical token allocation per GPU row (Q13, Q14)
 template <bool LAT>
-__device__ void phase1(Scn& c, int32_t t, Acc& acc) {
+static __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
   View& v = c.v;
   const Params& P = *c.P;
   const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
@@ -912,7 +912,7 @@ __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
 // P2: cross-row minima -- training gang (Q22) and LLM pipeline stages (Q11); only the
 // training and LLM functions (static list fDefL) are visited.
 template <bool LAT>
-__device__ void phase2(Scn& c, int32_t t, Acc& acc) {
+static __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
   View& v = c.v;
   const Params& P = *c.P;
   const int par = t & 1;
@@ -983,7 +983,7 @@ __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
 // (it is a mod-2^64 sum, order-free by construction, R8).
 
 template <bool LAT>
-__device__ void phase0_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
+static __device__ void phase0_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   View& v = c.v;
   const Params& P = *c.P;
   const int32_t* __restrict__ infl = v.fInfL;
@@ -1045,7 +1045,7 @@ __device__ void phase0_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
 }
 
 template <bool LAT>
-__device__ void phase1_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
+static __device__ void phase1_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   View& v = c.v;
   const Params& P = *c.P;
   const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
@@ -1148,7 +1148,7 @@ __device__ void phase1_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
 }
 
 template <bool LAT>
-__device__ void phase2_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
+static __device__ void phase2_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   View& v = c.v;
   const Params& P = *c.P;
   const int32_t* __restrict__ defl = v.fDefL;
@@ -1217,13 +1217,13 @@ __device__ void phase2_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
 // per-GPU "state" fold over the SLO residents, the capacity clamp) are segment shuffles.
 // B slots (fused batch) or one slot; r, stage minima and gangs come through base/stride.
 
-__device__ __forceinline__ int32_t a2_grow(int32_t r_last) {   // ceil(max(R_last,1) * 5/4)
+static __device__ __forceinline__ int32_t a2_grow(int32_t r_last) {   // ceil(max(R_last,1) * 5/4)
   const long long r = r_last < 1 ? 1 : r_last;
   return (int32_t)((r * 5 + 3) / 4);
 }
 
 template <bool LAT>
-__device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* rbase, size_t rstride,
+static __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* rbase, size_t rstride,
                             int32_t* bminb, size_t bstride, int32_t* gangb, size_t gstride,
                             int32_t* emaxb, Acc& acc) {
   View& v = c.v;
@@ -1429,7 +1429,7 @@ __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* rbase, 
 
 enum : int32_t { EV_DEP = 1, EV_OUT = 2, EV_IN = 4, EV_ARR = 8 };
 
-__device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, int32_t pf_ring) {
+static __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, int32_t pf_ring) {
   View& v = c.v;
   const Params& P = *c.P;
   const int32_t sec = t / P.SPS;
@@ -1585,7 +1585,7 @@ __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, int32_t
 // (cfg.flags bit2).  Separate instantiations, so the one-slot-per-second slot-model kernels
 // (C1-C4) carry neither the batch nor the period code.
 template <bool SMEM, int VAR>
-__device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem, int32_t sc, int32_t t0,
+static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem, int32_t sc, int32_t t0,
                              int32_t n_slots, int32_t n_req, const int32_t* req_scn,
                              const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid,
                              int K = 1, int crank = 0) {
@@ -1854,6 +1854,7 @@ k_run_cluster(Params Pin, int32_t t0, int32_t n_slots, int32_t n_req, const int3
                       out_iid, (int)csize, (int)crank);
 }
 
+#ifndef DILU_VARIANT_TU   // the init / snapshot kernels live in dilu_api.cu's unit only
 // Initialise every scenario's block at slot 0 (one CTA per scenario).
 __global__ void k_init(Params P) {
   const int32_t sc = blockIdx.x;
@@ -1969,5 +1970,6 @@ __global__ void k_snapshot(Params P, int32_t id_cap, int32_t* out_gpu, int32_t* 
     }
   }
 }
+#endif  // DILU_VARIANT_TU
 
 }  // namespace dilu
