@@ -403,9 +403,38 @@ static __device__ void kill_queue_entry_with_id(View& v, int32_t id) {
 
 // ---- placement (collective) --------------------------------------------------------
 
+// Placement primitives of the group (WARP = false: every thread of the CTA / cluster) or
+// of warp 0 alone (WARP = true: CTA engine, G <= WARP_PLACE_MAX -- scoring 64..256 GPUs
+// at 2..8 per lane beats three CTA barriers per attempt).
+constexpr int WARP_PLACE_MAX = 256;
+template <bool WARP> struct PlaceGrp;
+template <> struct PlaceGrp<false> {
+  static __device__ __forceinline__ int rank(const Scn& c) { return c.g.rank(); }
+  static __device__ __forceinline__ int size(const Scn& c) { return c.g.size(); }
+  static __device__ __forceinline__ bool leader(const Scn& c) { return c.g.leader(); }
+  static __device__ __forceinline__ void sync(const Scn& c) { c.g.sync(); }
+};
+template <> struct PlaceGrp<true> {
+  static __device__ __forceinline__ int rank(const Scn&) { return threadIdx.x; }
+  static __device__ __forceinline__ int size(const Scn&) { return 32; }
+  static __device__ __forceinline__ bool leader(const Scn&) { return threadIdx.x == 0; }
+  static __device__ __forceinline__ void sync(const Scn&) { __syncwarp(); }
+};
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, v, o);
+    v = y < v ? y : v;
+  }
+  return v;
+}
+
 // Algorithm 1 for one instance s with Principle 2's LLM split before a new
-// GPU (Q11).  All threads call; thread 0 commits.  Returns a uniform success flag.
+// GPU (Q11).  All threads of the placing group call; its leader commits.  Returns a
+// uniform success flag.
+template <bool WARP>
 static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
+  using PG = PlaceGrp<WARP>;
   View& v = c.v;
   const Params& P = *c.P;
   const int32_t f = v.iFunc[s];
@@ -413,7 +442,7 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
   const long long aM = (long long)P.aw * P.M, bQ = (long long)P.bw * P.Q;
   const unsigned long long MASK40 = (1ull << 40) - 1;
   unsigned long long best = ~0ull;
-  for (int32_t g = c.g.rank(); g < P.G; g += c.g.size()) {
+  for (int32_t g = PG::rank(c); g < P.G; g += PG::size(c)) {
     if (v.gExcl[g]) continue;
     const int32_t n = v.gN[g];
     unsigned long long key;
@@ -435,11 +464,11 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
     }
     best = key < best ? key : best;
   }
-  best = g_min_u64(c, best, red, ph);
+  best = WARP ? warp_min_u64(best) : g_min_u64(c, best, red, ph);
   const int tier = best == ~0ull ? 3 : (int)(best >> 62);
   if (tier <= 1) {
-    if (c.g.leader()) commit(c, s, (int32_t)(best & 0x3FFFFF), mem);
-    c.g.sync();
+    if (PG::leader(c)) commit(c, s, (int32_t)(best & 0x3FFFFF), mem);
+    PG::sync(c);
     return true;
   }
   if (v.fKind[f] == K_LLM && (P.flags & 1) && c.mode != M_EXCLUSIVE) {
@@ -451,7 +480,7 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
     bool okk = false;
     for (int r = 0; r < P.max_stages; ++r) {
       unsigned long long kk = ~0ull;
-      for (int32_t g = c.g.rank(); g < P.G; g += c.g.size()) {
+      for (int32_t g = PG::rank(c); g < P.G; g += PG::size(c)) {
         const int32_t n = v.gN[g];
         if (n == 0 || v.gExcl[g] || n >= RES) continue;
         bool dup = false;
@@ -464,7 +493,7 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
             ((unsigned long long)(0xFFFFFFFFu - (uint32_t)fr) << 32) | (uint32_t)g;
         kk = key < kk ? key : kk;
       }
-      kk = g_min_u64(c, kk, red, ph);
+      kk = WARP ? warp_min_u64(kk) : g_min_u64(c, kk, red, ph);
       if (kk == ~0ull) break;
       picked[r] = (int32_t)(kk & 0xFFFFFFFFu);
       pfree[r] = (int32_t)(0xFFFFFFFFu - (uint32_t)(kk >> 32));
@@ -473,7 +502,7 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
       if (sum >= mem) { okk = true; break; }
     }
     if (okk) {
-      if (c.g.leader()) {
+      if (PG::leader(c)) {
         int32_t left = mem;
         for (int j = 0; j < k; ++j) {
           const int32_t sh = pfree[j] < left ? pfree[j] : left;
@@ -481,13 +510,13 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
           left -= sh;
         }
       }
-      c.g.sync();
+      PG::sync(c);
       return true;
     }
   }
   if (tier == 2) {
-    if (c.g.leader()) commit(c, s, (int32_t)(best & 0x3FFFFF), mem);
-    c.g.sync();
+    if (PG::leader(c)) commit(c, s, (int32_t)(best & 0x3FFFFF), mem);
+    PG::sync(c);
     return true;
   }
   return false;
@@ -574,7 +603,9 @@ static __device__ int32_t next_attempt(Scn& c, int32_t q, int32_t qn, Acc& acc) 
 // Entered without a group barrier after B3 (the leader's serial event pass): only warp 0
 // (which contains the leader) reads the queue before the first barrier below, and it
 // broadcasts the queue length with the first attempt index.
+template <bool WARP>
 static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
+  using PG = PlaceGrp<WARP>;
   View& v = c.v;
   int32_t qn = 0;
   bool removed = false;                 // leader only
@@ -584,8 +615,8 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
     // request needing a real attempt (warp 0, 32 entries per step), gather its members
     // (leader); then a single group barrier.
     TSTART;
-    if (c.g.lead_warp()) {
-      if (c.g.leader() && prev >= 0) {
+    if (WARP || c.g.lead_warp()) {
+      if (PG::leader(c) && prev >= 0) {
         const int32_t n = v.qN[prev], f = v.qFunc[prev];
         for (int j = 0; j < prev_placed; ++j) {   // clear I* marks
           const int32_t s = c.members[j];
@@ -613,7 +644,7 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
       __syncwarp();
       if (prev < 0) qn = v.h[H_ERR] ? 0 : v.h[H_QLEN];   // after B3 (same warp)
       const int32_t e = next_attempt(c, q, qn, acc);
-      if (c.g.leader()) {
+      if (PG::leader(c)) {
         c.flag[0] = e;
         c.flag[1] = qn;
         if (e < qn) {                   // gang members, ascending id
@@ -627,7 +658,7 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
         }
       }
     }
-    c.g.sync();
+    PG::sync(c);
     TSTOP(17);
     q = c.g.K == 1 ? c.flag[0] : __ldcg(c.flag);
     qn = c.g.K == 1 ? c.flag[1] : __ldcg(c.flag + 1);
@@ -637,7 +668,7 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
     {
       TSTART;
       for (int j = 0; j < n; ++j) {
-        if (!place_one(c, red, ph, c.g.K == 1 ? c.members[j] : __ldcg(c.members + j))) break;
+        if (!place_one<WARP>(c, red, ph, c.g.K == 1 ? c.members[j] : __ldcg(c.members + j))) break;
         ++placed;
       }
       TSTOP(18);
@@ -646,7 +677,18 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
     prev_placed = placed;
     ++q;
   }
-  if (c.g.leader() && removed) compact_queue(v);
+  if (PG::leader(c) && removed) compact_queue(v);
+}
+
+// The placement pass by the cheapest group: warp 0 alone for CTA-engine scenarios with
+// few GPUs (then one CTA barrier publishes its commits), else the whole group.
+static __device__ void placement(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
+  if (c.g.K == 1 && c.P->G <= WARP_PLACE_MAX) {
+    if (threadIdx.x < 32) placement_pass<true>(c, red, ph, t, acc);
+    __syncthreads();
+  } else {
+    placement_pass<false>(c, red, ph, t, acc);
+  }
 }
 
 // ---- B5: pack GPU rows into 32-lane warp chunks by width class (1..32 lanes) ----------
@@ -1574,7 +1616,7 @@ static __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
   // step 5.  No barrier between: the pass starts with a warp-0 section (see there).  It
   // ends with a group barrier after the last commit; what follows it (the leader's queue
   // compaction) touches only the queue, which nothing reads before the next boundary.
-  placement_pass(c, red, ph, t, acc);
+  placement(c, red, ph, t, acc);
 }
 
 // ---------------------------------------------------------------------------- kernels
@@ -1643,7 +1685,7 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
       }
     }
     c.g.sync();
-    if (!v.h[H_ERR]) placement_pass(c, red, ph, t0, acc);
+    if (!v.h[H_ERR]) placement(c, red, ph, t0, acc);
     c.g.sync();
     for (int32_t j = c.g.rank(); j < n_req; j += c.g.size()) {
       if (req_scn[j] != sc) continue;
