@@ -396,7 +396,7 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
     // size does, the one with the fewest waves.
     const int S = cfg->n_scenarios > 0 ? cfg->n_scenarios : 1;
     int K = 0, best_waves = 0;
-    for (int k = want >= 16 ? 16 : (want >= 8 ? 8 : (want >= 4 ? 4 : (want >= 2 ? 2 : 1))); k >= 1; k /= 2) {
+    for (int k = want >= 16 ? 16 : (want < 1 ? 1 : want); k >= 1; --k) {   // any size 1..16
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3(k);
       lc.blockDim = dim3(s->threads);
