@@ -5,6 +5,7 @@ import ast
 import os
 import re
 
+import numpy as np
 import pytest
 
 import dilu_inputs as di
@@ -68,3 +69,40 @@ def test_product_package_does_not_touch_oracle():
                         assert not (node.module or "").startswith("oracle"), p
             if fn.endswith((".cu", ".cuh", ".h")):
                 assert "dilu_ref" not in open(p).read(), p
+
+
+def test_profiler_struct_layouts_match_header():
+    """dilu_prof_session / dilu_prof_out (include/dilu.h) and the generator's dtypes have
+    the same fields in the same order and size (both sides read the same bytes)."""
+    src = open(os.path.join(ROOT, "include", "dilu.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+
+    def names(struct):
+        body = re.search(r"typedef struct \{([^{}]*)\}\s*" + struct + ";", src).group(1)
+        out = []
+        for typ, decl in re.findall(r"(int32_t|double)\s+([^;]+);", body):
+            out += [(typ, n.strip()) for n in decl.split(",")]
+        return out
+    for struct, dt in (("dilu_prof_session", di.PROF_SESSION), ("dilu_prof_out", di.PROF_OUT)):
+        fs = names(struct)
+        assert [n for _, n in fs] == list(dt.names), struct
+        for (typ, n) in fs:
+            assert dt[n] == (np.dtype("<i4") if typ == "int32_t" else np.dtype("<f8")), (struct, n)
+
+
+def test_abi_argument_errors_without_gpu():
+    """Argument validation that needs no device: dilu_profile rejects n < 0 and null or
+    misaligned pointers; the latency / Alg.2 flags are validated with the config."""
+    import ctypes
+    import paper_2503_05130_b200 as pkg
+    L = pkg.lib()
+    assert L.dilu_profile(None, -1, None, None) == 1
+    assert L.dilu_profile(None, 5, None, None) == 1
+    assert L.dilu_profile(ctypes.c_void_p(8), 1, ctypes.c_void_p(12), None) == 1
+    assert L.dilu_profile(None, 0, None, None) == 0
+    wl = di.c1()
+    cfg = wl.cfg_array().copy()
+    cfg[di.CONFIG_FIELDS.index("flags")] |= 4 | 8
+    assert pkg.dilu_workspace_bytes(cfg) > 0                     # 1 s slots: fine
+    cfg[di.CONFIG_FIELDS.index("slot_ms")] = 8                   # not a multiple of 5
+    assert pkg.dilu_workspace_bytes(cfg) == 0

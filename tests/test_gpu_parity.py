@@ -343,3 +343,12 @@ def test_latency_fused_100ms(shape, monkeypatch):
     wl = di.scaled("C5b", 512, 60, 120, 360, 100, 400, [53, 54], max_instances=8192)
     latency_pair(with_flags(wl, 8), [1, 13, 386], id_cap=16384)
     latency_pair(with_flags(wl, 8 | 4), [1, 13, 386], id_cap=16384)
+
+
+def test_latency_requires_flag():
+    from paper_2503_05130_b200 import DiluError
+    gs = gpu_sim(di.c1())
+    gs.scale_step(5)
+    with pytest.raises(DiluError) as e:
+        gs.latency()
+    assert e.value.code == 1
