@@ -1,5 +1,7 @@
-import sys, numpy as np, torch
-sys.path.insert(0, '.')
+"""Per-scenario cycle counts of the C4 sweep (a -DDILU_PHASE_TIMING build via DILU_LIB),
+for the scheduling analysis in DESIGN.md s7: python tools/c4_scenario_cycles.py."""
+import os, sys, numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import dilu_inputs as di
 from paper_2503_05130_b200 import DiluSim, lib
 wl = di.c4(n_scenarios=4096)

@@ -1,3 +1,6 @@
+# Round-1 evidence: bench lines (C4, C5, C4 Alg.2, oracle arm), the ncu launch list and
+# ncu --set full captures of the C4 and C5 kernels, all under gpurun_out/r1b/.
+# Run on the GPU box: gpurun -- bash tools/collect_evidence.sh
 set -x
 mkdir -p gpurun_out/r1b
 python bench.py > gpurun_out/r1b/bench_c4.json 2> gpurun_out/r1b/bench_c4.err
