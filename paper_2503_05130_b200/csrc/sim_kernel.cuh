@@ -360,9 +360,14 @@ static __device__ int32_t enqueue(Scn& c, int32_t f, int32_t n) {
 static __device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
   View& v = c.v;
   if (v.h[H_FSTOP] < n) { v.h[H_ERR] = 6; return -1; }
-  if (v.h[H_QLEN] == c.P->I) compact_queue(v);
+  if (v.h[H_QLEN] == c.P->I) {
+    compact_queue(v);
+    v.h[H_QNEWPOS] = 0;               // positions moved: the next pass scans everything
+  }
   const int32_t first = v.h[H_NEXT_IID];
   const int32_t q = v.h[H_QLEN]++;
+  v.h[H_QLIVE] += 1;
+  if (v.h[H_QNEWPOS] < 0) v.h[H_QNEWPOS] = q;
   for (int32_t j = 0; j < n; ++j) {
     const int32_t s = v.fstack[--v.h[H_FSTOP]];
     v.iId[s] = v.h[H_NEXT_IID]++;
@@ -392,13 +397,18 @@ static __device__ void register_func(View& v, int32_t f, int32_t t, int32_t Tp) 
 
 static __device__ void kill_queue_entries_of(View& v, int32_t f) {
   const int32_t n = v.h[H_QLEN];
-  for (int32_t q = 0; q < n; ++q) if (v.qN[q] > 0 && v.qFunc[q] == f) v.qN[q] = 0;
+  for (int32_t q = 0; q < n; ++q)
+    if (v.qN[q] > 0 && v.qFunc[q] == f) { v.qN[q] = 0; v.h[H_QLIVE] -= 1; }
 }
 
 static __device__ void kill_queue_entry_with_id(View& v, int32_t id) {
   const int32_t n = v.h[H_QLEN];
   for (int32_t q = 0; q < n; ++q)
-    if (v.qN[q] > 0 && v.qFirst[q] <= id && id < v.qFirst[q] + v.qN[q]) { v.qN[q] = 0; return; }
+    if (v.qN[q] > 0 && v.qFirst[q] <= id && id < v.qFirst[q] + v.qN[q]) {
+      v.qN[q] = 0;
+      v.h[H_QLIVE] -= 1;
+      return;
+    }
 }
 
 // ---- placement (collective) --------------------------------------------------------
@@ -634,6 +644,7 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
             if (nst_of(v.iMeta[s]) > 1) acc.z->split += 1;
           }
           v.qN[prev] = 0;
+          v.h[H_QLIVE] -= 1;
           removed = true;
         } else {
           for (int j = 0; j < prev_placed; ++j) release(c, c.members[j]);  // rollback
@@ -642,7 +653,18 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
         }
       }
       __syncwarp();
-      if (prev < 0) qn = v.h[H_ERR] ? 0 : v.h[H_QLEN];   // after B3 (same warp)
+      if (prev < 0) {                   // pass start, after B3 (same warp)
+        qn = v.h[H_ERR] ? 0 : v.h[H_QLEN];
+        // Every request still queued at the end of the last pass fails on that pass's
+        // final state.  With no release since (same epoch) the state has only filled,
+        // so those requests fail again without rescoring: count them and start at the
+        // first request enqueued since (all of which are live).  Exact, DESIGN.md s5.
+        if (v.h[H_LASTEP] == v.h[H_EPOCH]) {
+          const int32_t np = v.h[H_QNEWPOS];
+          q = np < 0 ? qn : np;             // np == 0: positions moved, scan all
+          if (threadIdx.x == 0 && q > 0) acc.z->pfail += v.h[H_QLIVE] - (qn - q);
+        }
+      }
       const int32_t e = next_attempt(c, q, qn, acc);
       if (PG::leader(c)) {
         c.flag[0] = e;
@@ -677,7 +699,11 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
     prev_placed = placed;
     ++q;
   }
-  if (PG::leader(c) && removed) compact_queue(v);
+  if (PG::leader(c)) {
+    if (removed) compact_queue(v);
+    v.h[H_LASTEP] = v.h[H_EPOCH];
+    v.h[H_QNEWPOS] = -1;
+  }
 }
 
 // The placement pass by the cheapest group: warp 0 alone for CTA-engine scenarios with
@@ -1597,7 +1623,10 @@ static __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
         acc.z->sout += 1;
       } else if (ev & EV_IN) {
         const int32_t victim = v.fLt[f];        // highest live id (Q19)
-        if (st_of(v.iMeta[victim]) == ST_PEND) v.qN[v.iQ[victim]] = 0;   // its own request
+        if (st_of(v.iMeta[victim]) == ST_PEND) {     // its own request
+          v.qN[v.iQ[victim]] = 0;
+          v.h[H_QLIVE] -= 1;
+        }
         terminate(c, victim);
         acc.z->sin += 1;
       }
@@ -1905,7 +1934,7 @@ __global__ void k_init(Params P) {
   const int32_t* rows = P.funcs + (size_t)sc * P.F * 16;
   for (int k = threadIdx.x; k < H_WORDS; k += blockDim.x) v.h[k] = 0;
   __syncthreads();
-  if (threadIdx.x == 0) { v.h[H_FSTOP] = P.I; v.h[H_DIRTY] = 1; }
+  if (threadIdx.x == 0) { v.h[H_FSTOP] = P.I; v.h[H_DIRTY] = 1; v.h[H_LASTEP] = -1; v.h[H_QNEWPOS] = -1; }
   for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
     v.gR[g] = 0; v.gL[g] = 0; v.gU[g] = 0; v.gN[g] = 0; v.gExcl[g] = 0; v.gGrow[g] = 0;
     v.gRel[g] = 0;

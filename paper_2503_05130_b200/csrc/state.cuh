@@ -30,7 +30,9 @@ enum : int32_t { ST_FREE = 0, ST_PEND = 1, ST_PLACED = 2 };
 enum : int {
   H_NEXT_IID = 0, H_NLIVE, H_QLEN, H_NACT, H_SUMU, H_EPOCH, H_DIRTY, H_FSTOP, H_ERR,
   H_NEV, H_CCNT = 10 /*6*/, H_CBASE = 16 /*7*/, H_GBASE = 23 /*6*/, H_CCNT2 = 29 /*6*/,
-  H_RLN = 35 /* release-log entries appended */, H_NINF = 36, H_NDEF = 37, H_WORDS = 40
+  H_RLN = 35 /* release-log entries appended */, H_NINF = 36, H_NDEF = 37,
+  H_QLIVE = 38 /* live queue requests */, H_LASTEP = 39 /* release epoch at the last pass's end */,
+  H_QNEWPOS = 40 /* first request enqueued since the last pass, -1 if none */, H_WORDS = 44
 };
 
 // tally indices (match include/dilu.h)
