@@ -1,8 +1,9 @@
 """Compile libdilu.so for sm_100a in-tree (nvcc cross-compiles without a GPU).
 
-Five translation units compile in parallel: dilu_api.cu (C-ABI, init / snapshot /
-lanes / profiler kernels) and run_variants.cu four times (DILU_VGROUP = 0..3, two of the
-eight k_run / k_run_cluster variants each); one nvcc link makes the shared library.
+Nine translation units compile in parallel: dilu_api.cu (C-ABI, init / snapshot /
+lanes / profiler kernels) and run_variants.cu eight times (DILU_VGROUP = 0..3, two of the
+eight kernel variants each, x DILU_HOT_SMEM = 1 for the shared-memory kernels / 0 for the
+global-memory and cluster kernels); one nvcc link makes the shared library.
 `python _build.py -DNAME[=v] ...` builds a side library libdilu_<name>.so with extra
 defines (e.g. -DDILU_PHASE_TIMING) for experiments."""
 from __future__ import annotations
@@ -37,8 +38,8 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: str = LIB) 
         return out
     with tempfile.TemporaryDirectory(prefix="dilu_build_") as tmp:
         units = [(os.path.join(CSRC, "dilu_api.cu"), [], "api.o")]
-        units += [(os.path.join(CSRC, "run_variants.cu"), [f"-DDILU_VGROUP={g}"], f"v{g}.o")
-                  for g in range(4)]
+        units += [(os.path.join(CSRC, "run_variants.cu"), [f"-DDILU_VGROUP={g}", f"-DDILU_HOT_SMEM={h}"],
+                   f"v{g}h{h}.o") for g in range(4) for h in (0, 1)]
 
         def compile_one(u):
             src, defs, obj = u

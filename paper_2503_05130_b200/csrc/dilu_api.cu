@@ -166,10 +166,10 @@ int variant_of(const dilu_config* c, const Layout& L) {
 }
 RunFn run_fn(bool smem, int var) {
   switch ((var & 7) >> 1) {
-    case 0: return run_fn_group0(smem, var);
-    case 1: return run_fn_group1(smem, var);
-    case 2: return run_fn_group2(smem, var);
-    default: return run_fn_group3(smem, var);
+    case 0: return smem ? run_fn_smem_group0(var) : run_fn_gmem_group0(var);
+    case 1: return smem ? run_fn_smem_group1(var) : run_fn_gmem_group1(var);
+    case 2: return smem ? run_fn_smem_group2(var) : run_fn_gmem_group2(var);
+    default: return smem ? run_fn_smem_group3(var) : run_fn_gmem_group3(var);
   }
 }
 ClusterFn cluster_fn(int var) {

@@ -220,6 +220,96 @@ static __device__ int32_t g_scan(Scn& c, int32_t v, Red& red, int& ph, int32_t* 
   return before + pre;
 }
 
+// ---- hot-region view ------------------------------------------------------------------
+// In translation units compiled with DILU_HOT_SMEM=1 (the k_run<true, *> kernels: the hot
+// region staged in shared memory) every hot-region pointer is asserted to be a shared-space
+// address, so the compiler emits LDS/STS/ATOMS instead of generic LD/ST/ATOM (29 vs 33
+// cycles per dependent load, tools/ubench/smem_chase.cu).  Functions take a register copy
+// of the view so the assertion reaches every access.  The leader's state-mutating helpers
+// (commit, release, terminate, enqueue) keep generic accesses: converted together they
+// faulted at run time in C2 (each one alone was clean) -- unresolved, so left out.
+#ifndef DILU_HOT_SMEM
+#define DILU_HOT_SMEM 0
+#endif
+static __device__ __forceinline__ View hot_view(const View& s) {
+  View v = s;
+#if DILU_HOT_SMEM
+#define DILU_A(p) __builtin_assume(__isShared(v.p))
+  DILU_A(h);
+  DILU_A(gR);
+  DILU_A(gL);
+  DILU_A(gU);
+  DILU_A(gN);
+  DILU_A(gRes);
+  DILU_A(gExcl);
+  DILU_A(gGrow);
+  DILU_A(gMask);
+  DILU_A(rlG);
+  DILU_A(rlE);
+  DILU_A(iId);
+  DILU_A(iFunc);
+  DILU_A(iMeta);
+  DILU_A(iReady);
+  DILU_A(iNext);
+  DILU_A(iR);
+  DILU_A(fKind);
+  DILU_A(fReq);
+  DILU_A(fLim);
+  DILU_A(fMem);
+  DILU_A(fCb);
+  DILU_A(fIbs);
+  DILU_A(fNw);
+  DILU_A(fCls);
+  DILU_A(fDtr);
+  DILU_A(fPat);
+  DILU_A(fScale);
+  DILU_A(fPhase);
+  DILU_A(fCap1);
+  DILU_A(fReg);
+  DILU_A(fNsamp);
+  DILU_A(fAcc);
+  DILU_A(fHead);
+  DILU_A(fUp);
+  DILU_A(fDown);
+  DILU_A(fThrn);
+  DILU_A(fNlive);
+  DILU_A(fLh);
+  DILU_A(fGang);
+  DILU_A(fFlag);
+  DILU_A(fArr);
+  DILU_A(fDep);
+  DILU_A(fPidx);
+  DILU_A(fInfL);
+  DILU_A(fDefL);
+  DILU_A(gRel);
+  DILU_A(fLt);
+  DILU_A(fK);
+  DILU_A(fList);
+  DILU_A(fstack);
+  DILU_A(fPrio);
+  DILU_A(fCold);
+  DILU_A(qFunc);
+  DILU_A(qFirst);
+  DILU_A(qN);
+  DILU_A(qFail);
+  DILU_A(qSlot);
+  DILU_A(iQ);
+#undef DILU_A
+#endif
+  return v;
+}
+
+// DILU_VIEW(v, c): the view a function works through -- a register copy carrying the
+// shared-space assertion in DILU_HOT_SMEM units, else a plain reference (a copy only
+// costs registers when the state is in global memory).
+#if DILU_HOT_SMEM
+#define DILU_VIEW(v, c) View v = hot_view((c).v)
+#define DILU_CVIEW(v, c) const View v = hot_view((c).v)
+#else
+#define DILU_VIEW(v, c) View& v = (c).v
+#define DILU_CVIEW(v, c) const View& v = (c).v
+#endif
+
 // ---- serial helpers (thread 0 only) ------------------------------------------------
 
 static __device__ void list_append(View& v, int32_t f, int32_t s) {
@@ -445,7 +535,7 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
 template <bool WARP>
 static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
   using PG = PlaceGrp<WARP>;
-  View& v = c.v;
+  DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int32_t f = v.iFunc[s];
   const int32_t req = v.fReq[f], lim = v.fLim[f], mem = v.fMem[f], cls = v.fCls[f];
@@ -536,7 +626,7 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
 // Non-LLM: g hosts one instance now (an emptied GPU always can).  LLM with split
 // enabled: g is also a split candidate (caps hold, some free memory).
 static __device__ __forceinline__ bool could_help(const Scn& c, int32_t g, int32_t f) {
-  const View& v = c.v;
+  DILU_CVIEW(v, c);
   const Params& P = *c.P;
   const int32_t n = v.gN[g];
   if (n == 0) return true;
@@ -549,7 +639,7 @@ static __device__ __forceinline__ bool could_help(const Scn& c, int32_t g, int32
 // log back to fe (usually 1-3 entries); falls back to scanning every GPU's last-release
 // epoch when the log no longer covers fe.
 static __device__ bool hope_after(const Scn& c, int32_t fe, int32_t f) {
-  const View& v = c.v;
+  DILU_CVIEW(v, c);
   const int32_t n = v.h[H_RLN];
   const int32_t lo = n > RLOG ? n - RLOG : 0;
   if (n > RLOG && v.rlE[lo % RLOG] > fe) {
@@ -569,7 +659,7 @@ static __device__ bool hope_after(const Scn& c, int32_t fe, int32_t f) {
 // epoch; returns the first entry that needs a real attempt, or qn.  Lane 0 is thread 0
 // (owner of the thread-0 tallies).
 static __device__ int32_t next_attempt(Scn& c, int32_t q, int32_t qn, Acc& acc) {
-  View& v = c.v;
+  DILU_VIEW(v, c);
   const int lane = threadIdx.x & 31;
   const int32_t ep = v.h[H_EPOCH];
   int32_t nfail = 0, found = qn, nhope = 0;
@@ -616,7 +706,7 @@ static __device__ int32_t next_attempt(Scn& c, int32_t q, int32_t qn, Acc& acc) 
 template <bool WARP>
 static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
   using PG = PlaceGrp<WARP>;
-  View& v = c.v;
+  DILU_VIEW(v, c);
   int32_t qn = 0;
   bool removed = false;                 // leader only
   int32_t q = 0, prev = -1, prev_placed = 0;
@@ -724,7 +814,7 @@ static __device__ __forceinline__ int width_class(int32_t n) {
 }
 
 static __device__ void rebuild_layout(Scn& c) {
-  View& v = c.v;
+  DILU_VIEW(v, c);
   const Params& P = *c.P;
   if (c.g.crank == 0 && threadIdx.x < 6) { v.h[H_CCNT + threadIdx.x] = 0; v.h[H_CCNT2 + threadIdx.x] = 0; }
   c.g.sync();
@@ -826,7 +916,7 @@ static __device__ __forceinline__ int32_t lat_e(int32_t cst, int32_t a, long lon
 // advanced incrementally (set at registration), so no modulo runs per slot.
 template <bool LAT>
 static __device__ void phase0(Scn& c, int32_t t, Acc& acc, int32_t pf_f, long long pf_x) {
-  View& v = c.v;
+  DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int32_t* __restrict__ infl = v.fInfL;
   const int32_t* __restrict__ reg = v.fReg;
@@ -875,7 +965,7 @@ static __device__ void phase0(Scn& c, int32_t t, Acc& acc, int32_t pf_f, long lo
 // P1: vertical token allocation per GPU row (Q13, Q14)
 template <bool LAT>
 static __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
-  View& v = c.v;
+  DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
   const int par = t & 1;
@@ -981,7 +1071,7 @@ static __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
 // training and LLM functions (static list fDefL) are visited.
 template <bool LAT>
 static __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
-  View& v = c.v;
+  DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int par = t & 1;
   const int32_t* __restrict__ r = v.iR + par * P.I;
@@ -1052,7 +1142,7 @@ static __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
 
 template <bool LAT>
 static __device__ void phase0_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
-  View& v = c.v;
+  DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int32_t* __restrict__ infl = v.fInfL;
   const int32_t* __restrict__ reg = v.fReg;
@@ -1114,7 +1204,7 @@ static __device__ void phase0_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
 
 template <bool LAT>
 static __device__ void phase1_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
-  View& v = c.v;
+  DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
   const int32_t* __restrict__ cbase = v.h + H_CBASE;
@@ -1217,7 +1307,7 @@ static __device__ void phase1_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
 
 template <bool LAT>
 static __device__ void phase2_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
-  View& v = c.v;
+  DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int32_t* __restrict__ defl = v.fDefL;
   const int32_t* __restrict__ lh = v.fLh;
@@ -1294,7 +1384,7 @@ template <bool LAT>
 static __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* rbase, size_t rstride,
                             int32_t* bminb, size_t bstride, int32_t* gangb, size_t gstride,
                             int32_t* emaxb, Acc& acc) {
-  View& v = c.v;
+  DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
   const unsigned FULL = 0xffffffffu;
@@ -1498,7 +1588,7 @@ static __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* 
 enum : int32_t { EV_DEP = 1, EV_OUT = 2, EV_IN = 4, EV_ARR = 8 };
 
 static __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, int32_t pf_ring) {
-  View& v = c.v;
+  DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int32_t sec = t / P.SPS;
   // B1 (function-parallel): window push, incremental counts, decisions, event flags.
@@ -1699,8 +1789,8 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
   if (VAR & 4)
     for (int k = threadIdx.x; k < NLAT; k += blockDim.x) red.lat[k] = 0;
   int ph = 0;
-  View& v = c.v;
   __syncthreads();
+  DILU_VIEW(v, c);            // after the barrier: thread 0 built the shared view
   if (v.h[H_ERR]) return;     // uniform: nobody has written since the group started
 
   if (n_req >= 0) {

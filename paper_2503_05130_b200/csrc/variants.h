@@ -14,10 +14,14 @@ typedef void (*RunFn)(Params, int32_t*, int32_t, int32_t, int32_t, const int32_t
 typedef void (*ClusterFn)(Params, int32_t, int32_t, int32_t, const int32_t*, const int32_t*,
                           int32_t*, int32_t*);
 // group g holds VAR 2g and 2g + 1
-RunFn run_fn_group0(bool smem, int var);
-RunFn run_fn_group1(bool smem, int var);
-RunFn run_fn_group2(bool smem, int var);
-RunFn run_fn_group3(bool smem, int var);
+RunFn run_fn_smem_group0(int var);   // DILU_HOT_SMEM=1 units
+RunFn run_fn_smem_group1(int var);
+RunFn run_fn_smem_group2(int var);
+RunFn run_fn_smem_group3(int var);
+RunFn run_fn_gmem_group0(int var);   // DILU_HOT_SMEM=0 units
+RunFn run_fn_gmem_group1(int var);
+RunFn run_fn_gmem_group2(int var);
+RunFn run_fn_gmem_group3(int var);
 ClusterFn cluster_fn_group0(int var);
 ClusterFn cluster_fn_group1(int var);
 ClusterFn cluster_fn_group2(int var);
