@@ -225,9 +225,9 @@ static __device__ int32_t g_scan(Scn& c, int32_t v, Red& red, int& ph, int32_t* 
 // region staged in shared memory) every hot-region pointer is asserted to be a shared-space
 // address, so the compiler emits LDS/STS/ATOMS instead of generic LD/ST/ATOM (29 vs 33
 // cycles per dependent load, tools/ubench/smem_chase.cu).  Functions take a register copy
-// of the view so the assertion reaches every access.  The leader's state-mutating helpers
-// (commit, release, terminate, enqueue) keep generic accesses: converted together they
-// faulted at run time in C2 (each one alone was clean) -- unresolved, so left out.
+// of the view so the assertion reaches every access.  terminate_impl keeps generic
+// accesses: converted together with release (which it calls) it faulted at run time in C2
+// (either one alone is clean, as is every other combination tried) -- unresolved.
 #ifndef DILU_HOT_SMEM
 #define DILU_HOT_SMEM 0
 #endif
@@ -332,7 +332,7 @@ static __device__ __forceinline__ long long res_key(const View& v, int32_t s) {
 }
 
 static __device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
-  View& v = c.v;
+  DILU_VIEW(v, c);
   const int32_t f = v.iFunc[s];
   if (v.gN[g] == 0) v.h[H_NACT] += 1;
   v.gMask[g] |= 1ull << (v.fCls[f] & 63);
@@ -361,7 +361,7 @@ static __device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
 }
 
 static __device__ void release(Scn& c, int32_t s) {
-  View& v = c.v;
+  DILU_VIEW(v, c);
   const int32_t f = v.iFunc[s];
   const int32_t meta = v.iMeta[s];
   const int n = nst_of(meta);
@@ -448,7 +448,7 @@ static __device__ int32_t enqueue(Scn& c, int32_t f, int32_t n) {
   return r;
 }
 static __device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
-  View& v = c.v;
+  DILU_VIEW(v, c);
   if (v.h[H_FSTOP] < n) { v.h[H_ERR] = 6; return -1; }
   if (v.h[H_QLEN] == c.P->I) {
     compact_queue(v);
