@@ -915,7 +915,7 @@ static __device__ __forceinline__ int32_t lat_e(int32_t cst, int32_t a, long lon
 // A_f(t) = (pat[p_f][(t + phase_f) mod T_pat] * scale_f) >> 10; the pattern index is
 // advanced incrementally (set at registration), so no modulo runs per slot.
 template <bool LAT>
-static __device__ void phase0(Scn& c, int32_t t, Acc& acc, int32_t pf_f, long long pf_x) {
+static __device__ void phase0(Scn& c, int32_t t, Acc& acc) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int32_t* __restrict__ infl = v.fInfL;
@@ -936,9 +936,7 @@ static __device__ void phase0(Scn& c, int32_t t, Acc& acc, int32_t pf_f, long lo
     if (!reg[f]) continue;
     const int32_t idx = pidx[f];
     pidx[f] = idx + 1 == Tp ? 0 : idx + 1;
-    // the first item's pattern value was prefetched at slot start (valid unless f was
-    // registered at this boundary: pf_f is only set for functions registered before it)
-    const long long x = f == pf_f ? pf_x : __ldg(gpat + (size_t)fpat[f] * Tp + idx);
+    const long long x = __ldg(gpat + (size_t)fpat[f] * Tp + idx);
     const int32_t A = (int32_t)((x * fscale[f]) >> 10);
     acc.nfun += 1;
     facc[f] += A;
@@ -1587,7 +1585,7 @@ static __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* 
 
 enum : int32_t { EV_DEP = 1, EV_OUT = 2, EV_IN = 4, EV_ARR = 8 };
 
-static __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, int32_t pf_ring) {
+static __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int32_t sec = t / P.SPS;
@@ -1630,7 +1628,7 @@ static __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
             const long long cu = (long long)thr * cap1, cd = (long long)(thr - 1) * cap1;
             int32_t du = val > cu, dd = val < cd;
             if (ns >= W) {
-              const int32_t old = f == lo ? pf_ring : ring[head];   // prefetched at slot start
+              const int32_t old = ring[head];
               du -= old > cu; dd -= old < cd;
             }
             fup[f] += du;
@@ -1826,26 +1824,13 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
 #else
 #define TICK(slot) do { } while (0)
 #endif
-      int32_t pf_f = -1;                    // prefetch this thread's first P0 pattern value
-      long long pf_x = 0;
-      int32_t pf_ring = 0;                  // ... and, at a boundary, its first B1 ring word
-      if (t % P.SPS == 0) {
-        const int32_t per = (P.F + c.g.size() - 1) / c.g.size();
-        const int32_t f0 = c.g.rank() * per;
-        if (f0 < P.F && v.fReg[f0]) pf_ring = v.ring[(size_t)f0 * P.W + v.fHead[f0]];
-      }
-      if (!fused) {
-        const int32_t k = c.g.rank();
-        if (k < v.h[H_NINF]) {
-          const int32_t f = v.fInfL[k];
-          if (v.fReg[f]) { pf_f = f; pf_x = __ldg(P.pat + (size_t)v.fPat[f] * P.Tp + v.fPidx[f]); }
-        }
-      }
+      // (no cross-phase prefetch of the B1 ring word or the P0 pattern value: holding them
+      // in registers across the boundary cost 8.5 % of C4's step)
       if (t % P.SPS == 0) {
         // no barrier here: B1 touches only the per-function window fields, which P2(t-1)
         // never reads, and B1's own count barrier orders P2(t-1) before B3 mutates state
         TICK(0);
-        boundary(c, red, ph, t, acc, pf_ring);
+        boundary(c, red, ph, t, acc);
         TICK(1);
         if (v.h[H_ERR]) break;
       }
@@ -1880,7 +1865,7 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
         t += B - 1;
         continue;
       }
-      phase0<lat>(c, t, acc, pf_f, pf_x);
+      phase0<lat>(c, t, acc);
       if (c.g.leader()) {
         const long long na = v.h[H_NACT];
         acc.z->act += na;
