@@ -272,6 +272,8 @@ static __device__ __forceinline__ View hot_view(const View& s) {
   DILU_A(fUp);
   DILU_A(fDown);
   DILU_A(fThrn);
+  DILU_A(fOld);
+  DILU_A(fPv);
   DILU_A(fNlive);
   DILU_A(fLh);
   DILU_A(fGang);
@@ -302,6 +304,18 @@ static __device__ __forceinline__ View hot_view(const View& s) {
 // DILU_VIEW(v, c): the view a function works through -- a register copy carrying the
 // shared-space assertion in DILU_HOT_SMEM units, else a plain reference (a copy only
 // costs registers when the state is in global memory).
+// Asynchronous 4-byte global -> shared copies (no register staging): the next second's
+// evicted ring sample (B1) and the next slot's pattern value (P0) land in the hot state
+// while the slot runs, so neither global load sits on a phase's critical path.  Each thread
+// consumes only what it issued (same function mapping every slot) after cp.async.wait_all.
+static __device__ __forceinline__ void cp_async4(int32_t* sdst, const int32_t* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(s), "l"(gsrc) : "memory");
+}
+static __device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 #if DILU_HOT_SMEM
 #define DILU_VIEW(v, c) View v = hot_view((c).v)
 #define DILU_CVIEW(v, c) const View v = hot_view((c).v)
@@ -482,6 +496,7 @@ static __device__ void register_func(View& v, int32_t f, int32_t t, int32_t Tp) 
   v.fReg[f] = 1;
   v.fNsamp[f] = 0; v.fAcc[f] = 0; v.fHead[f] = 0; v.fUp[f] = 0; v.fDown[f] = 0;
   v.fThrn[f] = -1;
+  v.fPv[f] = -1;                     // no prefetched pattern value for the first slot
   v.fPidx[f] = (int32_t)(((long long)t + v.fPhase[f]) % Tp);   // arrivals index for slot t
 }
 
@@ -931,12 +946,23 @@ static __device__ void phase0(Scn& c, int32_t t, Acc& acc) {
   int32_t* __restrict__ r = v.iR + (t & 1) * P.I;
   const int32_t* __restrict__ gpat = P.pat;
   const int32_t Tp = P.Tp, ninf = v.h[H_NINF];
+#if DILU_HOT_SMEM
+  cp_async_wait_all();
+#endif
   for (int32_t k = c.g.rank(); k < ninf; k += c.g.size()) {
     const int32_t f = infl[k];
     if (!reg[f]) continue;
     const int32_t idx = pidx[f];
-    pidx[f] = idx + 1 == Tp ? 0 : idx + 1;
-    const long long x = __ldg(gpat + (size_t)fpat[f] * Tp + idx);
+    const int32_t nidx = idx + 1 == Tp ? 0 : idx + 1;
+    pidx[f] = nidx;
+    const int32_t* prow = gpat + (size_t)fpat[f] * Tp;
+#if DILU_HOT_SMEM
+    const int32_t pv = v.fPv[f];           // landed since the last slot (waited above)
+    const long long x = pv >= 0 ? pv : __ldg(prow + idx);
+    cp_async4(v.fPv + f, prow + nidx);      // next slot's value
+#else
+    const long long x = __ldg(prow + idx);
+#endif
     const int32_t A = (int32_t)((x * fscale[f]) >> 10);
     acc.nfun += 1;
     facc[f] += A;
@@ -1609,6 +1635,9 @@ static __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) 
   const int32_t per = (P.F + c.g.size() - 1) / c.g.size();
   const int32_t lo = c.g.rank() * per, hi = min(P.F, lo + per);
   int32_t cnt = 0;
+#if DILU_HOT_SMEM
+  cp_async_wait_all();                              // this thread's fOld / fPv copies landed
+#endif
   for (int32_t f = lo; f < hi; ++f) {
     const int32_t kind = fkind[f];
     int32_t ev = 0;
@@ -1628,14 +1657,22 @@ static __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) 
             const long long cu = (long long)thr * cap1, cd = (long long)(thr - 1) * cap1;
             int32_t du = val > cu, dd = val < cd;
             if (ns >= W) {
+#if DILU_HOT_SMEM
+              const int32_t old = W > 1 ? v.fOld[f] : ring[head];   // prefetched last second
+#else
               const int32_t old = ring[head];
+#endif
               du -= old > cu; dd -= old < cd;
             }
             fup[f] += du;
             fdown[f] += dd;
           }
           ring[head] = val;
-          fhead[f] = head + 1 == W ? 0 : head + 1;
+          const int32_t nhead = head + 1 == W ? 0 : head + 1;
+          fhead[f] = nhead;
+#if DILU_HOT_SMEM
+          if (W > 1) cp_async4(v.fOld + f, ring + nhead);        // next second's evictee
+#endif
           fns[f] = ns + 1;
           facc[f] = 0;
         }
@@ -1942,6 +1979,9 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
       }
   }
   if (SMEM) {
+#if DILU_HOT_SMEM
+    cp_async_wait_all();             // in-flight prefetches land before the write-back
+#endif
     __syncthreads();
     const int4* src = reinterpret_cast<const int4*>(smem);
     int4* dst = reinterpret_cast<int4*>(gblock);
@@ -2040,7 +2080,7 @@ __global__ void k_init(Params P) {
     // R5: cap1 = (1000/slot_ms) * floor(req_tok / c_b) * IBS
     v.fCap1[f] = is_inf(kind) ? (long long)P.SPS * (((long long)req * P.slot_ms) / r[6]) * r[2] : 0;
     v.fReg[f] = 0; v.fNsamp[f] = 0; v.fAcc[f] = 0; v.fHead[f] = 0; v.fUp[f] = 0; v.fDown[f] = 0;
-    v.fThrn[f] = -1; v.fNlive[f] = 0; v.fLh[f] = -1; v.fLt[f] = -1;
+    v.fThrn[f] = -1; v.fOld[f] = 0; v.fPv[f] = -1; v.fNlive[f] = 0; v.fLh[f] = -1; v.fLt[f] = -1;
     v.fGang[f] = BIG; v.fGang[P.F + f] = BIG; v.fFlag[f] = 0; v.fK[f] = 0; v.fList[f] = 0;
     v.fArr[f] = r[11]; v.fDep[f] = r[12]; v.fPidx[f] = 0;
   }

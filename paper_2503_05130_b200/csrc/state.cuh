@@ -49,7 +49,7 @@ struct Layout {
   size_t iId, iFunc, iMeta, iReady, iG, iSh0, iShare, iNext, iR, iBmin, fstack;
   size_t fKind, fPrio, fReq, fLim, fMem, fCb, fIbs, fNw, fCold, fCls, fDtr, fPat, fScale,
       fPhase, fCap1;
-  size_t fReg, fNsamp, fAcc, fHead, fUp, fDown, fThrn, fNlive, fLh, fLt, fGang, fFlag, fK,
+  size_t fReg, fNsamp, fAcc, fHead, fUp, fDown, fThrn, fOld, fPv, fNlive, fLh, fLt, fGang, fFlag, fK,
       fList, fArr, fDep, fPidx, fInfL, fDefL;
   size_t qFunc, qFirst, qN, qFail, qSlot, iQ;
   size_t rB, bB, gB;       // per-batch-slot r, LLM stage minimum, training gang (B > 1 only)
@@ -82,7 +82,9 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B 
   L.fCap1 = take(8 * (size_t)F);
   L.fReg = take(4 * (size_t)F); L.fNsamp = take(4 * (size_t)F); L.fAcc = take(4 * (size_t)F);
   L.fHead = take(4 * (size_t)F); L.fUp = take(4 * (size_t)F); L.fDown = take(4 * (size_t)F);
-  L.fThrn = take(4 * (size_t)F); L.fNlive = take(4 * (size_t)F); L.fLh = take(4 * (size_t)F);
+  L.fThrn = take(4 * (size_t)F);
+  L.fOld = take(4 * (size_t)F); L.fPv = take(4 * (size_t)F);   // cp.async landing slots
+  L.fNlive = take(4 * (size_t)F); L.fLh = take(4 * (size_t)F);
   L.fGang = take(4 * 2 * (size_t)F); L.fFlag = take(4 * (size_t)F);
   L.fArr = take(4 * (size_t)F); L.fDep = take(4 * (size_t)F); L.fPidx = take(4 * (size_t)F);
   L.fInfL = take(4 * (size_t)F); L.fDefL = take(4 * (size_t)F);
@@ -127,7 +129,7 @@ struct View {
   int32_t *fKind, *fPrio, *fReq, *fLim, *fMem, *fCb, *fIbs, *fNw, *fCold, *fCls, *fDtr, *fPat,
       *fScale, *fPhase;
   int64_t* fCap1;
-  int32_t *fReg, *fNsamp, *fAcc, *fHead, *fUp, *fDown, *fThrn, *fNlive, *fLh, *fLt, *fGang,
+  int32_t *fReg, *fNsamp, *fAcc, *fHead, *fUp, *fDown, *fThrn, *fOld, *fPv, *fNlive, *fLh, *fLt, *fGang,
       *fFlag, *fK, *fList, *fArr, *fDep, *fPidx, *fInfL, *fDefL;
   int32_t *qFunc, *qFirst, *qN, *qFail, *qSlot, *iQ;
   int32_t *rB, *bB, *gB;
@@ -152,7 +154,7 @@ inline View make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
   P32(fKind); P32(fPrio); P32(fReq); P32(fLim); P32(fMem); P32(fCb); P32(fIbs); P32(fNw);
   P32(fCold); P32(fCls); P32(fDtr); P32(fPat); P32(fScale); P32(fPhase);
   v.fCap1 = reinterpret_cast<int64_t*>(hot + L.fCap1);
-  P32(fReg); P32(fNsamp); P32(fAcc); P32(fHead); P32(fUp); P32(fDown); P32(fThrn); P32(fNlive);
+  P32(fReg); P32(fNsamp); P32(fAcc); P32(fHead); P32(fUp); P32(fDown); P32(fThrn); P32(fOld); P32(fPv); P32(fNlive);
   P32(fLh); P32(fLt); P32(fGang); P32(fFlag); P32(fK); P32(fList); P32(fArr); P32(fDep);
   P32(fPidx); P32(fInfL); P32(fDefL);
   P32(qFunc); P32(qFirst); P32(qN); P32(qFail); P32(qSlot); P32(iQ);
