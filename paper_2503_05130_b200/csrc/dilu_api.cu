@@ -360,6 +360,7 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   P.phi_out = cfg->phi_out; P.phi_in = cfg->phi_in; P.min_inst = cfg->min_instances;
   P.max_stages = cfg->max_llm_stages; P.flags = cfg->flags; P.Tp = cfg->pattern_len;
   P.T_slot = 1000LL * cfg->slot_ms;
+  P.ovl = 0;
 
   s->engine = choose_engine(cfg);
   s->parts = choose_parts();
@@ -453,9 +454,19 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   if (per_sm < 1) return fail(s, DILU_E_CUDA, "kernel cannot be resident with %d threads", s->threads);
   const long long cap = (long long)per_sm * n_sm;
   s->grid = (int)(cfg->n_scenarios < cap ? cfg->n_scenarios : cap);
+  // Overlapped slots: warp 0 places while the other warps run P0/P1/P2.
+  // Exact only if nothing placed in a slot is warm in it, i.e. every cold start >= 1 slot.
+  {
+    bool cold_ok = true;
+    for (size_t i = 0; i < S * F && cold_ok; ++i)
+      if (h_funcs[i].kind != -1 && h_funcs[i].cold_slots < 1) cold_ok = false;
+    const char* e = getenv("DILU_NO_OVL");
+    P.ovl = cold_ok && variant_of(cfg, s->L) == 0 && G <= WARP_PLACE_MAX && s->threads >= 64 &&
+            !(e && atoi(e));
+  }
   if (getenv("DILU_VERBOSE"))
-    fprintf(stderr, "dilu: cta engine threads=%d smem=%d hot=%zu per_sm=%d grid=%d\n", s->threads,
-            (int)s->use_smem, s->L.hot_bytes, per_sm, s->grid);
+    fprintf(stderr, "dilu: cta engine threads=%d smem=%d hot=%zu per_sm=%d grid=%d ovl=%d\n", s->threads,
+            (int)s->use_smem, s->L.hot_bytes, per_sm, s->grid, P.ovl);
   if (const char* e = getenv("DILU_GRID")) {   // test/tuning hook: resident scenarios
     const int v = atoi(e);
     if (v >= 1 && v < s->grid) s->grid = v;

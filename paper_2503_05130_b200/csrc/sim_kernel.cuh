@@ -39,6 +39,7 @@ struct Params {
   Layout L;
   int32_t S, G, F, I, W, M, Q, aw, bw, slot_ms, SPS, phi_out, phi_in, min_inst, max_stages,
       flags, Tp;
+  int32_t ovl;               // overlapped slots: CTA engine, VAR 0, G <= 256, cold >= 1
   int64_t T_slot;
 };
 
@@ -141,12 +142,13 @@ static __device__ __forceinline__ void cluster_sync_all() {
 
 struct Grp {
   int K, crank, cph;
+  int off;                   // threads [0, off) sit out (overlapped slots: warp 0 places)
   unsigned long long* gu;    // [2][16] cluster scratch (u64)
   int32_t* gi;               // [2][16] cluster scratch (i32)
-  __device__ int rank() const { return crank * blockDim.x + threadIdx.x; }
-  __device__ int size() const { return K * blockDim.x; }
-  __device__ int wrank() const { return (crank * blockDim.x + threadIdx.x) >> 5; }
-  __device__ int nwarps() const { return (K * blockDim.x) >> 5; }
+  __device__ int rank() const { return crank * blockDim.x + threadIdx.x - off; }
+  __device__ int size() const { return K * blockDim.x - off; }
+  __device__ int wrank() const { return (crank * blockDim.x + threadIdx.x - off) >> 5; }
+  __device__ int nwarps() const { return (K * blockDim.x - off) >> 5; }
   __device__ bool leader() const { return crank == 0 && threadIdx.x == 0; }
   __device__ bool lead_warp() const { return crank == 0 && threadIdx.x < 32; }
   __device__ void sync() const {
@@ -356,9 +358,11 @@ static __device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
   v.h[H_SUMU] += share;
   int32_t* res = v.gRes + (size_t)g * RES;
   int pos = v.gN[g];
-  const long long k = res_key(v, s);
-  while (pos > 0 && res_key(v, res[pos - 1]) > k) { res[pos] = res[pos - 1]; --pos; }
-  res[pos] = s;
+  if (!c.P->ovl) {            // keep (prio, id) order now ...
+    const long long k = res_key(v, s);
+    while (pos > 0 && res_key(v, res[pos - 1]) > k) { res[pos] = res[pos - 1]; --pos; }
+  }                           // ... or append (overlapped slots: rows below gNs never move
+  res[pos] = s;               // while P1 reads them; the next repack sorts the row)
   v.gN[g] += 1;
   const int32_t meta = v.iMeta[s];
   const int k0 = nst_of(meta);
@@ -477,7 +481,7 @@ static __device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
     v.iId[s] = v.h[H_NEXT_IID]++;
     v.iFunc[s] = f;
     v.iMeta[s] = ST_PEND;
-    v.iReady[s] = 0;
+    v.iReady[s] = BIG;               // not ready until placed (read racily in overlapped slots)
     v.iQ[s] = q;                      // request index (single-instance kills are O(1))
     if (j == 0) v.qSlot[q] = s;
     for (int k = 0; k < MAXST; ++k) v.iG[s * MAXST + k] = -1;
@@ -835,6 +839,19 @@ static __device__ void rebuild_layout(Scn& c) {
   c.g.sync();
   for (int32_t g = c.g.rank(); g < P.G; g += c.g.size()) {
     const int32_t n = v.gN[g];
+    if (P.ovl && n > 1) {     // overlapped slots append commits: restore (prio, id) order
+      int32_t* res = v.gRes + (size_t)g * RES;
+      long long kp = res_key(v, res[0]);
+      for (int j = 1; j < n; ++j) {
+        const int32_t s = res[j];
+        const long long k = res_key(v, s);
+        if (k > kp) { kp = k; continue; }
+        int pos = j;
+        while (pos > 0 && res_key(v, res[pos - 1]) > k) { res[pos] = res[pos - 1]; --pos; }
+        res[pos] = s;
+      }
+    }
+    v.gNs[g] = n;
     if (n > 0) atomicAdd(&v.h[H_CCNT + width_class(n)], 1);
   }
   c.g.sync();
@@ -997,7 +1014,9 @@ static __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
   int32_t* bmin = v.iBmin + par * P.I;
   int32_t* gang = v.fGang + par * P.F;
   const int32_t* __restrict__ grow = v.gGrow;
-  const int32_t* __restrict__ gn = v.gN;
+  // row sizes as of the last repack: in overlapped slots warp 0 appends (cold) residents
+  // beyond them while this runs; rows below gNs never move (commit)
+  const int32_t* __restrict__ gn = v.gNs;
   const int32_t* __restrict__ gres = v.gRes;
   const int32_t* __restrict__ meta_ = v.iMeta;
   const int32_t* __restrict__ ready = v.iReady;
@@ -1611,7 +1630,9 @@ static __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* 
 
 enum : int32_t { EV_DEP = 1, EV_OUT = 2, EV_IN = 4, EV_ARR = 8 };
 
-static __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
+// Returns whether a placement pass is due.  ovl (overlapped slots): the pass is left to
+// the caller, which runs it in warp 0 beside P0/P1/P2.
+static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, bool ovl = false) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int32_t sec = t / P.SPS;
@@ -1717,9 +1738,9 @@ static __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) 
     int32_t pos = g_scan(c, cnt, red, ph, &total);
     for (int32_t f = lo; f < hi && cnt; ++f)
       if (fflag[f]) { v.fList[pos++] = f; --cnt; }
+    c.g.sync();                                     // the event list is complete before B3
   }
   const int32_t need_pass = total > 0 || v.h[H_QLEN] > 0;   // uniform: QLEN only changes in B3/placement
-  if (total > 0) c.g.sync();                       // the event list is complete before B3
 #ifdef DILU_PHASE_TIMING
   long long bt0 = clock64();
   if (c.g.leader()) acc.z->st[14] -= bt0;   // st[14] += (end of B3) - (end of B1)
@@ -1728,7 +1749,7 @@ static __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) 
 #ifdef DILU_PHASE_TIMING
     if (c.g.leader()) acc.z->st[14] += bt0;
 #endif
-    return;
+    return false;
   }
   // B3: apply in the paper's order (steps 2, 3, 4), thread 0
   if (c.g.leader() && total > 0) {
@@ -1764,13 +1785,16 @@ static __device__ void boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) 
       else for (int32_t j = 0; j < P.min_inst && !v.h[H_ERR]; ++j) enqueue(c, f, 1);
     }
   }
+  if (ovl && any) __syncthreads();   // B3's state changes before P0/P1/P2 and the repack
 #ifdef DILU_PHASE_TIMING
   if (c.g.leader()) acc.z->st[14] += clock64();
 #endif
+  if (ovl) return true;
   // step 5.  No barrier between: the pass starts with a warp-0 section (see there).  It
   // ends with a group barrier after the last commit; what follows it (the leader's queue
   // compaction) touches only the queue, which nothing reads before the next boundary.
   placement(c, red, ph, t, acc);
+  return true;
 }
 
 // ---------------------------------------------------------------------------- kernels
@@ -1802,6 +1826,7 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
   c.g.K = K;
   c.g.crank = crank;
   c.g.cph = 0;
+  c.g.off = 0;
   c.g.gu = P.gscratch + (size_t)sc * GSCR;
   c.g.gi = reinterpret_cast<int32_t*>(c.g.gu + 32);
   if (K == 1) {
@@ -1863,6 +1888,49 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
 #endif
       // (no cross-phase prefetch of the B1 ring word or the P0 pattern value: holding them
       // in registers across the boundary cost 8.5 % of C4's step)
+      // overlapped slot: warp 0 runs the placement pass while warps 1.. run
+      // P0/P1/P2 over the state after B3.  Exact when every cold start is >= 1 slot (the
+      // host's P.ovl): what the pass commits is cold in this slot, so P0/P1/P2 never count
+      // it; pending instances read as not ready (iReady = BIG), rows only grow past gNs.
+      const bool ovl = !fused && !alg2 && !lat && P.ovl;
+      if (ovl) {
+        bool pass = false;
+        TICK(0);
+        if (t % P.SPS == 0) {
+          pass = boundary(c, red, ph, t, acc, true);   // B1 + B3 (+ barrier)
+          if (v.h[H_ERR]) break;                                  // uniform after B3's barrier
+        }
+        TICK(1);
+        if (v.h[H_DIRTY]) {
+          rebuild_layout(c);
+          if (c.g.leader()) acc.z->st[S_LAYOUT] += 1;
+        }
+        TICK(2);
+        if (threadIdx.x < 32) {
+          if (pass) placement_pass<true>(c, red, ph, t, acc);
+          if (c.g.leader()) {        // after the pass: this slot's active set
+            const long long na = v.h[H_NACT];
+            acc.z->act += na;
+            acc.z->memu += na * P.M - v.h[H_SUMU];
+            acc.z->rows += P.G;
+            acc.z->maxa = na > acc.z->maxa ? na : acc.z->maxa;
+            acc.z->st[S_SLOT] += 1;
+          }
+          TICK(3);
+        } else {
+          Scn cw = c;
+          cw.g.off = 32;
+          const int nb = (int)blockDim.x - 32;
+          phase0<false>(cw, t, acc);
+          asm volatile("bar.sync 1, %0;" :: "r"(nb) : "memory");
+          phase1<false>(cw, t, acc);
+          asm volatile("bar.sync 1, %0;" :: "r"(nb) : "memory");
+          phase2<false>(cw, t, acc);
+        }
+        __syncthreads();     // join: B1(t+1) resets the window fields P0(t) accumulates
+        TICK(4);
+        continue;
+      }
       if (t % P.SPS == 0) {
         // no barrier here: B1 touches only the per-function window fields, which P2(t-1)
         // never reads, and B1's own count barrier orders P2(t-1) before B3 mutates state
@@ -2051,7 +2119,7 @@ __global__ void k_init(Params P) {
   __syncthreads();
   if (threadIdx.x == 0) { v.h[H_FSTOP] = P.I; v.h[H_DIRTY] = 1; v.h[H_LASTEP] = -1; v.h[H_QNEWPOS] = -1; }
   for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
-    v.gR[g] = 0; v.gL[g] = 0; v.gU[g] = 0; v.gN[g] = 0; v.gExcl[g] = 0; v.gGrow[g] = 0;
+    v.gR[g] = 0; v.gL[g] = 0; v.gU[g] = 0; v.gN[g] = 0; v.gNs[g] = 0; v.gExcl[g] = 0; v.gGrow[g] = 0;
     v.gRel[g] = 0;
     v.gMask[g] = 0;
   }

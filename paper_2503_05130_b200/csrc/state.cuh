@@ -45,7 +45,7 @@ struct Layout {
   int32_t G, F, I, W, B;   // B: slots per fused batch between second boundaries (1 = unfused)
   // byte offsets inside one block
   size_t hdr;
-  size_t gR, gL, gU, gN, gRes, gExcl, gGrow, gMask, gRel, rlG, rlE;
+  size_t gR, gL, gU, gN, gNs, gRes, gExcl, gGrow, gMask, gRel, rlG, rlE;
   size_t iId, iFunc, iMeta, iReady, iG, iSh0, iShare, iNext, iR, iBmin, fstack;
   size_t fKind, fPrio, fReq, fLim, fMem, fCb, fIbs, fNw, fCold, fCls, fDtr, fPat, fScale,
       fPhase, fCap1;
@@ -69,7 +69,9 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B 
   // hot region: touched every slot -> staged in shared memory when it fits
   L.hdr = take(H_WORDS * 4);
   L.gR = take(4 * (size_t)G); L.gL = take(4 * (size_t)G); L.gU = take(4 * (size_t)G);
-  L.gN = take(4 * (size_t)G); L.gRes = take(4 * (size_t)G * RES);
+  L.gN = take(4 * (size_t)G);
+  L.gNs = take(4 * (size_t)G);          // row sizes at the last repack (overlapped slots, s5)
+  L.gRes = take(4 * (size_t)G * RES);
   L.gExcl = take(4 * (size_t)G); L.gGrow = take(4 * (size_t)G);
   L.gMask = take(8 * (size_t)G);        // bit (affinity_class & 63) per resident class
   L.rlG = take(4 * RLOG); L.rlE = take(4 * RLOG);
@@ -122,7 +124,7 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B 
 // Typed view of one scenario's block (pointers into smem or global).
 struct View {
   int32_t* h;
-  int32_t *gR, *gL, *gU, *gN, *gRes, *gExcl, *gGrow, *gRel, *rlG, *rlE;
+  int32_t *gR, *gL, *gU, *gN, *gNs, *gRes, *gExcl, *gGrow, *gRel, *rlG, *rlE;
   unsigned long long* gMask;
   int32_t *iId, *iFunc, *iMeta, *iReady, *iSh0, *iShare, *iNext, *iR, *iBmin, *fstack;
   int16_t* iG;
@@ -146,7 +148,7 @@ inline View make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
   View v;
 #define P32(name) v.name = reinterpret_cast<int32_t*>((L.name < L.hot_bytes ? hot : b) + L.name)
   v.h = reinterpret_cast<int32_t*>(hot + L.hdr);
-  P32(gR); P32(gL); P32(gU); P32(gN); P32(gRes); P32(gExcl); P32(gGrow); P32(gRel); P32(rlG); P32(rlE);
+  P32(gR); P32(gL); P32(gU); P32(gN); P32(gNs); P32(gRes); P32(gExcl); P32(gGrow); P32(gRel); P32(rlG); P32(rlE);
   v.gMask = reinterpret_cast<unsigned long long*>((L.gMask < L.hot_bytes ? hot : b) + L.gMask);
   P32(iId); P32(iFunc); P32(iMeta); P32(iReady); P32(iSh0); P32(iShare); P32(iNext); P32(iR);
   v.iG = reinterpret_cast<int16_t*>((L.iG < L.hot_bytes ? hot : b) + L.iG);

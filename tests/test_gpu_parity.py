@@ -94,7 +94,7 @@ def test_c4_sample_full_hour():
     run_pair(wl, [3600], snap=False)
 
 
-@pytest.mark.parametrize("mode", ["cta_threads64", "cta_threads1024", "cta_no_smem", "lanes_p4",
+@pytest.mark.parametrize("mode", ["cta_threads64", "cta_threads1024", "cta_no_smem", "cta_no_ovl", "lanes_p4",
                                   "lanes_p16", "lanes_p8"])
 def test_launch_shape_invariance(mode, monkeypatch):
     """Both engines and several launch shapes give bit-identical results (45 scenarios:
@@ -109,6 +109,8 @@ def test_launch_shape_invariance(mode, monkeypatch):
         monkeypatch.setenv("DILU_THREADS", "1024")
     elif shape == "no_smem":
         monkeypatch.setenv("DILU_NO_SMEM", "1")
+    elif shape == "no_ovl":          # placement pass not overlapped with P0/P1/P2
+        monkeypatch.setenv("DILU_NO_OVL", "1")
     elif shape.startswith("p"):
         monkeypatch.setenv("DILU_PARTS", shape[1:])
     run_pair(wl, [1, 599], id_cap=2048)
