@@ -487,6 +487,7 @@ static __device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
     for (int k = 0; k < MAXST; ++k) v.iG[s * MAXST + k] = -1;
     v.iBmin[s] = BIG;
     v.iBmin[c.P->I + s] = BIG;
+    if (c.P->SPS == 1) v.iR[c.P->I + s] = BIG;   // stage-minimum half of iR (phase1)
     list_append(v, f, s);
     v.fNlive[f] += 1;
     v.h[H_NLIVE] += 1;
@@ -960,7 +961,7 @@ static __device__ void phase0(Scn& c, int32_t t, Acc& acc) {
   const int32_t* __restrict__ nxt = v.iNext;
   const int32_t* __restrict__ meta = v.iMeta;
   const int32_t* __restrict__ ready = v.iReady;
-  int32_t* __restrict__ r = v.iR + (t & 1) * P.I;
+  int32_t* __restrict__ r = v.iR + (P.SPS == 1 ? 0 : (t & 1)) * P.I;   // see phase1
   const int32_t* __restrict__ gpat = P.pat;
   const int32_t Tp = P.Tp, ninf = v.h[H_NINF];
 #if DILU_HOT_SMEM
@@ -1010,8 +1011,13 @@ static __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
   const Params& P = *c.P;
   const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
   const int par = t & 1;
-  const int32_t* __restrict__ r = v.iR + par * P.I;
-  int32_t* bmin = v.iBmin + par * P.I;
+  // With one slot per second every slot starts with B1's counting barrier (or an
+  // overlapped slot's join), which orders P2(t) before P0/P1(t+1): r needs one buffer and
+  // the LLM stage minima use the other half of iR (shared memory) instead of the cold
+  // double buffer iBmin.
+  const bool one = P.SPS == 1;
+  const int32_t* __restrict__ r = v.iR + (one ? 0 : par) * P.I;
+  int32_t* bmin = one ? v.iR + P.I : v.iBmin + par * P.I;
   int32_t* gang = v.fGang + par * P.F;
   const int32_t* __restrict__ grow = v.gGrow;
   // row sizes as of the last repack: in overlapped slots warp 0 appends (cold) residents
@@ -1117,8 +1123,9 @@ static __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int par = t & 1;
-  const int32_t* __restrict__ r = v.iR + par * P.I;
-  int32_t* bmin = v.iBmin + par * P.I;
+  const bool one = P.SPS == 1;          // buffers as in phase1
+  const int32_t* __restrict__ r = v.iR + (one ? 0 : par) * P.I;
+  int32_t* bmin = one ? v.iR + P.I : v.iBmin + par * P.I;
   int32_t* gang = v.fGang + par * P.F;
   const int32_t* __restrict__ defl = v.fDefL;
   const int32_t* __restrict__ reg = v.fReg;
@@ -1983,7 +1990,9 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
       TICK(3);
       if (alg2) {
         const int par = t & 1;
-        phase1_alg2<lat>(c, t, 1, v.iR + par * P.I, 0, v.iBmin + par * P.I, 0, v.fGang + par * P.F, 0,
+        const bool one = P.SPS == 1;         // buffers as in phase1
+        phase1_alg2<lat>(c, t, 1, v.iR + (one ? 0 : par) * P.I, 0, one ? v.iR + P.I : v.iBmin + par * P.I, 0,
+                         v.fGang + par * P.F, 0,
                          v.iEmax + par * P.I, acc);
       } else {
         phase1<lat>(c, t, acc);
@@ -2128,7 +2137,7 @@ __global__ void k_init(Params P) {
     v.iId[s] = -1; v.iFunc[s] = -1; v.iMeta[s] = ST_FREE; v.iReady[s] = 0; v.iNext[s] = -1;
     for (int k = 0; k < MAXST; ++k) { v.iG[s * MAXST + k] = -1; v.iShare[s * MAXST + k] = 0; }
     v.iSh0[s] = 0;
-    v.iR[s] = 0; v.iR[P.I + s] = 0; v.iBmin[s] = BIG; v.iBmin[P.I + s] = BIG;
+    v.iR[s] = 0; v.iR[P.I + s] = P.SPS == 1 ? BIG : 0; v.iBmin[s] = BIG; v.iBmin[P.I + s] = BIG;
     v.fstack[s] = P.I - 1 - s;
   }
   const int32_t mode = P.scen[sc * 4 + 3];
