@@ -736,13 +736,16 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
     // (leader); then a single group barrier.
     TSTART;
     if (WARP || c.g.lead_warp()) {
+      if (WARP && prev >= 0)                  // clear I* marks: every lane clears a stride
+        for (int32_t g = threadIdx.x; g < c.P->G; g += 32) v.gExcl[g] = 0;   // (no iG loads)
       if (PG::leader(c) && prev >= 0) {
         const int32_t n = v.qN[prev], f = v.qFunc[prev];
-        for (int j = 0; j < prev_placed; ++j) {   // clear I* marks
-          const int32_t s = c.members[j];
-          const int ns = nst_of(v.iMeta[s]);
-          for (int k = 0; k < ns; ++k) v.gExcl[v.iG[s * MAXST + k]] = 0;
-        }
+        if (!WARP)
+          for (int j = 0; j < prev_placed; ++j) {   // clear I* marks
+            const int32_t s = c.members[j];
+            const int ns = nst_of(v.iMeta[s]);
+            for (int k = 0; k < ns; ++k) v.gExcl[v.iG[s * MAXST + k]] = 0;
+          }
         if (prev_placed == n) {
           const int32_t cold = v.fCold[f];
           for (int j = 0; j < n; ++j) {
