@@ -3,7 +3,7 @@
 # C5 kernels, all under gpurun_out/r1f/.
 # Run on the GPU box: gpurun -- bash tools/collect_evidence.sh
 set -x
-D=gpurun_out/r1h
+D=gpurun_out/r1i
 mkdir -p $D
 python bench.py > $D/bench_c4.json 2> $D/bench_c4.err
 python bench.py --workload C5 > $D/bench_c5.json 2> $D/bench_c5.err
