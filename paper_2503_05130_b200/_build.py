@@ -1,7 +1,7 @@
 """Compile libdilu.so for sm_100a in-tree (nvcc cross-compiles without a GPU).
 
 Nine translation units compile in parallel: dilu_api.cu (C-ABI, init / snapshot /
-lanes / profiler kernels) and run_variants.cu eight times (DILU_VGROUP = 0..3, two of the
+profiler kernels) and run_variants.cu eight times (DILU_VGROUP = 0..3, two of the
 eight kernel variants each, x DILU_HOT_SMEM = 1 for the shared-memory kernels / 0 for the
 global-memory and cluster kernels); one nvcc link makes the shared library.
 `python _build.py -DNAME[=v] ...` builds a side library libdilu_<name>.so with extra
@@ -18,7 +18,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libdilu.so")
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = [os.path.join(CSRC, n) for n in ("dilu_api.cu", "run_variants.cu", "sim_kernel.cuh",
-                                           "state.cuh", "sim_lanes.cuh", "profile.cuh",
+                                           "state.cuh", "profile.cuh",
                                            "variants.h")]
 HEADER = os.path.join(ROOT, "include", "dilu.h")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -66,5 +66,5 @@ if __name__ == "__main__":
     verbose = "verbose" in sys.argv or "-v" in sys.argv
     extra = [a for a in sys.argv[1:] if a.startswith("-D")]
     out = LIB if not extra else os.path.join(HERE, "libdilu_" + "_".join(
-        e[2:].lower().split("=")[0] for e in extra) + ".so")
+        e[2:].lower().replace("=", "_") for e in extra) + ".so")
     print(build(force=True, verbose=verbose, extra=extra, out=out))

@@ -15,7 +15,6 @@
 
 #include "../../include/dilu.h"
 #include "sim_kernel.cuh"
-#include "sim_lanes.cuh"
 #include "profile.cuh"
 #include "variants.h"
 
@@ -23,13 +22,10 @@ using namespace dilu;
 
 struct dilu_sim {
   dilu_config cfg;
-  int engine;          // 0: CTA per scenario, 1: lanes (32 scenarios per CTA), 2: cluster per scenario
+  int engine;          // 0: CTA per scenario, 2: cluster per scenario
   int K;               // cluster engine: CTAs per scenario
-  int parts;           // lanes engine: warps per scenario group
   Layout L;
   Params P;
-  lanes::LLayout LL;
-  lanes::LParams LP;
   cudaStream_t stream;
   uint8_t* ws;
   size_t ws_bytes;
@@ -124,17 +120,14 @@ bool check_inputs(const dilu_config* c, const dilu_scenario* scen, const dilu_fu
 #undef BAD
 }
 
-// Engine choice (a pure function of the config and the DILU_ENGINE / DILU_PARTS hooks).
-// Default: the CTA engine for every config (measured fastest); the lanes
-// engine (32 scenarios per CTA) is available for small scenarios and is parity-tested.
+// Engine choice (a pure function of the config and the DILU_ENGINE hook): one CTA per
+// scenario for G <= 256 (state staged in shared memory), a thread-block cluster per
+// scenario above.
 int choose_engine(const dilu_config* c) {
   int e = c->gpus_per_scenario > 256 ? 2 : 0;   // large scenarios: a cluster each
   if (const char* v = getenv("DILU_ENGINE")) {
     if (!strcmp(v, "cta")) e = 0;
     if (!strcmp(v, "cluster")) e = 2;
-    if (!strcmp(v, "lanes") && c->gpus_per_scenario <= 256 && c->max_funcs <= 4096 &&
-        c->max_instances <= 8192 && !(c->flags & 12))    // lanes: no Alg.2, no latency
-      e = 1;
   }
   return e;
 }
@@ -149,14 +142,6 @@ int choose_batch(const dilu_config* c) {
     if (x >= 1 && x <= 16) b = x < sps ? x : sps;
   }
   return b < 1 ? 1 : b;
-}
-int choose_parts() {
-  int p = 8;
-  if (const char* v = getenv("DILU_PARTS")) {
-    const int x = atoi(v);
-    if (x == 4 || x == 8 || x == 16) p = x;
-  }
-  return p;
 }
 
 // Kernel variant for a handle: bit0 fused sub-second batches, bit1 literal Alg.2 periods,
@@ -185,20 +170,11 @@ Carve carve(const dilu_config* c, const Layout& L) {
   Carve k;
   size_t o = 0;
   const size_t S = c->n_scenarios, F = c->max_funcs;
-  const int engine = choose_engine(c);
   k.funcs = o; o = up(o + S * F * sizeof(dilu_func));
   k.pat = o; o = up(o + (size_t)c->n_patterns * c->pattern_len * 4);
   k.scen = o; o = up(o + S * 16);
-  if (engine == 1) {
-    const lanes::LLayout LL = lanes::make_llayout(c->gpus_per_scenario, c->max_funcs,
-                                                  c->max_instances, c->window_s, choose_parts());
-    const size_t ngroups = (S + lanes::LN - 1) / lanes::LN;
-    k.state = o; o = up(o + ngroups * LL.bytes);
-    k.ring = o;                      // rings live inside the interleaved group state
-  } else {
-    k.state = o; o = up(o + S * L.bytes);
-    k.ring = o; o = up(o + S * F * c->window_s * 4);
-  }
+  k.state = o; o = up(o + S * L.bytes);
+  k.ring = o; o = up(o + S * F * c->window_s * 4);
   k.tally = o; o = up(o + S * NT * 8);
   k.stats = o; o = up(o + S * NSTAT * 8);
   k.gscr = o; o = up(o + S * GSCR * 8);
@@ -261,16 +237,8 @@ dilu_status launch_run(dilu_sim* s, int32_t n_slots, int32_t n_req, const int32_
     if (rc) return rc;
     return cuda_check(s, cudaGetLastError(), "k_run_cluster");
   }
-  if (s->engine == 1) {
-    switch (s->parts) {
-      case 4: lanes::k_lanes<4><<<grid, block, 0, s->stream>>>(s->LP, s->d_next, s->t, n_slots, n_req, rs, rf, og, oi); break;
-      case 16: lanes::k_lanes<16><<<grid, block, 0, s->stream>>>(s->LP, s->d_next, s->t, n_slots, n_req, rs, rf, og, oi); break;
-      default: lanes::k_lanes<8><<<grid, block, 0, s->stream>>>(s->LP, s->d_next, s->t, n_slots, n_req, rs, rf, og, oi); break;
-    }
-  } else {
-    const RunFn fn = run_fn(s->use_smem, variant_of(&s->cfg, s->L));
-    fn<<<grid, block, s->use_smem ? s->L.hot_bytes : 0, s->stream>>>(s->P, s->d_next, s->t, n_slots, n_req, rs, rf, og, oi);
-  }
+  const RunFn fn = run_fn(s->use_smem, variant_of(&s->cfg, s->L));
+  fn<<<grid, block, s->use_smem ? s->L.hot_bytes : 0, s->stream>>>(s->P, s->d_next, s->t, n_slots, n_req, rs, rf, og, oi);
   return cuda_check(s, cudaGetLastError(), "k_run launch");
 }
 
@@ -363,24 +331,8 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   P.ovl = 0;
 
   s->engine = choose_engine(cfg);
-  s->parts = choose_parts();
   int dev = 0;
   cudaGetDevice(&dev);
-  if (s->engine == 1) {
-    lanes::LParams& Q = s->LP;
-    s->LL = lanes::make_llayout(cfg->gpus_per_scenario, cfg->max_funcs, cfg->max_instances,
-                                cfg->window_s, s->parts);
-    Q.funcs = P.funcs; Q.pat = P.pat; Q.scen = P.scen; Q.state = P.state; Q.tally = P.tally;
-    Q.stats = P.stats; Q.L = s->LL;
-    Q.S = P.S; Q.ngroups = (P.S + lanes::LN - 1) / lanes::LN; Q.G = P.G; Q.F = P.F; Q.I = P.I;
-    Q.W = P.W; Q.M = P.M; Q.Q = P.Q; Q.aw = P.aw; Q.bw = P.bw; Q.slot_ms = P.slot_ms;
-    Q.SPS = P.SPS; Q.phi_out = P.phi_out; Q.phi_in = P.phi_in; Q.min_inst = P.min_inst;
-    Q.max_stages = P.max_stages; Q.flags = P.flags; Q.Tp = P.Tp; Q.T_slot = P.T_slot;
-    s->threads = 32 * s->parts;
-    s->use_smem = false;
-    s->grid = Q.ngroups;       // one persistent CTA per group: every group resident
-    return dilu_sim_reset(s);
-  }
   if (s->engine == 2) {
     s->threads = 1024;
     s->use_smem = false;
@@ -479,10 +431,10 @@ dilu_status dilu_sim_reset(dilu_sim* s) {
   if (s->status == DILU_E_CUDA) return DILU_E_STATE;
   s->status = DILU_OK;
   s->t = 0;
-  if (s->engine == 1)
-    lanes::k_lanes_init<<<s->LP.ngroups, lanes::LN, 0, s->stream>>>(s->LP);
-  else
-    k_init<<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P);
+  dilu_status rc = cuda_check(s, cudaMemsetAsync(s->P.state, 0, (size_t)s->cfg.n_scenarios * s->L.bytes, s->stream),
+                              "state reset");
+  if (rc) return rc;
+  k_init<<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P);
   return cuda_check(s, cudaGetLastError(), "k_init launch");
 }
 
@@ -528,8 +480,7 @@ dilu_status dilu_scale_step(dilu_sim* s, int32_t n_slots) {
 dilu_status dilu_metrics(dilu_sim* s, int64_t* per_scenario, int64_t* sum) {
   if (!s) return DILU_E_USAGE;
   if (s->status == DILU_E_CUDA) return DILU_E_STATE;
-  k_sum_err<<<1, 32, 0, s->stream>>>(s->P, s->d_sum, s->engine != 1);
-  if (s->engine == 1) lanes::k_lanes_errs<<<1, 32, 0, s->stream>>>(s->LP, s->d_sum + NT);
+  k_sum_err<<<1, 32, 0, s->stream>>>(s->P, s->d_sum, 1);
   dilu_status rc = cuda_check(s, cudaGetLastError(), "k_sum launch");
   if (rc) return rc;
   int64_t host_sum[NT + 1];
@@ -554,11 +505,7 @@ dilu_status dilu_snapshot(dilu_sim* s, int32_t id_cap, int32_t* d_gpu, int32_t* 
   if (!s) return DILU_E_USAGE;
   if (s->status == DILU_E_CUDA) return DILU_E_STATE;
   if (id_cap < 0 || (id_cap > 0 && !d_inst && d_gpu == nullptr)) return fail(s, DILU_E_USAGE, "snapshot: bad args");
-  if (s->engine == 1)
-    lanes::k_lanes_snapshot<<<s->LP.ngroups, lanes::LN, 0, s->stream>>>(s->LP, id_cap, d_gpu,
-                                                                         id_cap > 0 ? d_inst : nullptr);
-  else
-    k_snapshot<<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P, id_cap, d_gpu, id_cap > 0 ? d_inst : nullptr);
+  k_snapshot<<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P, id_cap, d_gpu, id_cap > 0 ? d_inst : nullptr);
   dilu_status rc = cuda_check(s, cudaGetLastError(), "k_snapshot launch");
   if (rc) return rc;
   return cuda_check(s, cudaStreamSynchronize(s->stream), "snapshot sync");

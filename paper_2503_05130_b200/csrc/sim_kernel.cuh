@@ -21,6 +21,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "state.cuh"
 
@@ -128,6 +129,16 @@ static __device__ __forceinline__ int32_t block_scan_i32(int32_t v, Red& r, int&
   return before + x - v;
 }
 
+#ifdef DILU_BOUNDS
+constexpr int DILU_ID_MEMBERS = 80;   // index of "members" in DILU_ARRAY_NAMES
+static __device__ __noinline__ void dilu_oob(int id, long long j, long long n) {
+  const char* names[] = {DILU_ARRAY_NAMES};
+  printf("DILU_BOUNDS: %s[%lld] outside [0, %lld) (block %d thread %d)\n",
+         id >= 0 && id <= DILU_ID_MEMBERS ? names[id] : "?", j, n, (int)blockIdx.x, (int)threadIdx.x);
+  __trap();
+}
+#endif
+
 // ------------------------------------------------------------------ groups
 //
 // The threads that run one scenario: one CTA (K = 1), or a thread-block cluster of K
@@ -162,7 +173,7 @@ struct Scn {
   View& v;                   // lives in shared memory (one per CTA), not in registers
   const Params* P;
   Grp g;
-  int32_t* members;          // gang member slots of the request being placed (group-visible)
+  DPN(int32_t) members;      // gang member slots of the request being placed (group-visible, [64])
   int32_t* flag;             // group-visible broadcast word
   Acc0* z;                   // leader tallies (shared)
   const int32_t* frow;       // this scenario's input function rows [F][16]
@@ -235,7 +246,7 @@ static __device__ int32_t g_scan(Scn& c, int32_t v, Red& red, int& ph, int32_t* 
 #endif
 static __device__ __forceinline__ View hot_view(const View& s) {
   View v = s;
-#if DILU_HOT_SMEM
+#if DILU_HOT_SMEM && !defined(DILU_BOUNDS)
 #define DILU_A(p) __builtin_assume(__isShared(v.p))
   DILU_A(h);
   DILU_A(gR);
@@ -318,7 +329,7 @@ static __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-#if DILU_HOT_SMEM
+#if DILU_HOT_SMEM && !defined(DILU_BOUNDS)
 #define DILU_VIEW(v, c) View v = hot_view((c).v)
 #define DILU_CVIEW(v, c) const View v = hot_view((c).v)
 #else
@@ -356,7 +367,7 @@ static __device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
   v.gL[g] += v.fLim[f];
   v.gU[g] += share;
   v.h[H_SUMU] += share;
-  int32_t* res = v.gRes + (size_t)g * RES;
+  DPN(int32_t) res = v.gRes + (size_t)g * RES;
   int pos = v.gN[g];
   if (!c.P->ovl) {            // keep (prio, id) order now ...
     const long long k = res_key(v, s);
@@ -390,7 +401,7 @@ static __device__ void release(Scn& c, int32_t s) {
     v.gL[g] -= v.fLim[f];
     v.gU[g] -= sh;
     v.h[H_SUMU] -= sh;
-    int32_t* res = v.gRes + (size_t)g * RES;
+    DPN(int32_t) res = v.gRes + (size_t)g * RES;
     int j = 0;
     const int nr = v.gN[g];
     while (j < nr && res[j] != s) ++j;
@@ -421,13 +432,23 @@ static __device__ void terminate(Scn& c, int32_t s) {
   TSTOP(15);
 }
 static __device__ void terminate_impl(Scn& c, int32_t s) {
+#ifdef DILU_TERM_SMEM
+  DILU_VIEW(v, c);
+#else
   View& v = c.v;
+#endif
   const int32_t f = v.iFunc[s];
   if (st_of(v.iMeta[s]) == ST_PLACED) {
     const int32_t ep = ++v.h[H_EPOCH];   // room was freed: queued failures may now succeed
     const int ns = nst_of(v.iMeta[s]);
     for (int k = 0; k < ns; ++k) {
       const int32_t g = v.iG[s * MAXST + k];
+#ifdef DILU_TERM_PROBE
+      if (g < 0 || g >= c.P->G)
+        printf("TERM_PROBE scn %d s %d k %d ns %d g %d meta %d id %d func %d gRel %p iG %p iMeta %p sv.iG %p\n",
+               c.scn_id, s, k, ns, g, v.iMeta[s], v.iId[s], v.iFunc[s], (void*)v.gRel, (void*)v.iG,
+               (void*)v.iMeta, (void*)c.v.iG);
+#endif
       v.gRel[g] = ep;
       const int32_t slot = v.h[H_RLN]++ % RLOG;
       v.rlG[slot] = g;
@@ -573,7 +594,7 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
     } else {
       const int32_t R = v.gR[g] + req, Lm = v.gL[g] + lim, U = v.gU[g] + mem;
       if (!(R <= c.om && Lm <= c.ga && U <= P.M && n < RES)) continue;
-      const int32_t* res = v.gRes + (size_t)g * RES;
+      const DPN(int32_t) res = v.gRes + (size_t)g * RES;
       // affinity: the class bitmask rules most GPUs out exactly; scan on a hit
       int aff = 0;
       if ((v.gMask[g] >> (cls & 63)) & 1ull)
@@ -844,7 +865,7 @@ static __device__ void rebuild_layout(Scn& c) {
   for (int32_t g = c.g.rank(); g < P.G; g += c.g.size()) {
     const int32_t n = v.gN[g];
     if (P.ovl && n > 1) {     // overlapped slots append commits: restore (prio, id) order
-      int32_t* res = v.gRes + (size_t)g * RES;
+      DPN(int32_t) res = v.gRes + (size_t)g * RES;
       long long kp = res_key(v, res[0]);
       for (int j = 1; j < n; ++j) {
         const int32_t s = res[j];
@@ -954,17 +975,17 @@ template <bool LAT>
 static __device__ void phase0(Scn& c, int32_t t, Acc& acc) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
-  const int32_t* __restrict__ infl = v.fInfL;
-  const int32_t* __restrict__ reg = v.fReg;
-  const int32_t* __restrict__ fpat = v.fPat;
-  const int32_t* __restrict__ fscale = v.fScale;
-  int32_t* __restrict__ pidx = v.fPidx;
-  int32_t* __restrict__ facc = v.fAcc;
-  const int32_t* __restrict__ lh = v.fLh;
-  const int32_t* __restrict__ nxt = v.iNext;
-  const int32_t* __restrict__ meta = v.iMeta;
-  const int32_t* __restrict__ ready = v.iReady;
-  int32_t* __restrict__ r = v.iR + (P.SPS == 1 ? 0 : (t & 1)) * P.I;   // see phase1
+  DP(const int32_t) infl = v.fInfL;
+  DP(const int32_t) reg = v.fReg;
+  DP(const int32_t) fpat = v.fPat;
+  DP(const int32_t) fscale = v.fScale;
+  DP(int32_t) pidx = v.fPidx;
+  DP(int32_t) facc = v.fAcc;
+  DP(const int32_t) lh = v.fLh;
+  DP(const int32_t) nxt = v.iNext;
+  DP(const int32_t) meta = v.iMeta;
+  DP(const int32_t) ready = v.iReady;
+  DP(int32_t) r = v.iR + (P.SPS == 1 ? 0 : (t & 1)) * P.I;   // see phase1
   const int32_t* __restrict__ gpat = P.pat;
   const int32_t Tp = P.Tp, ninf = v.h[H_NINF];
 #if DILU_HOT_SMEM
@@ -1019,27 +1040,27 @@ static __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
   // the LLM stage minima use the other half of iR (shared memory) instead of the cold
   // double buffer iBmin.
   const bool one = P.SPS == 1;
-  const int32_t* __restrict__ r = v.iR + (one ? 0 : par) * P.I;
-  int32_t* bmin = one ? v.iR + P.I : v.iBmin + par * P.I;
-  int32_t* gang = v.fGang + par * P.F;
-  const int32_t* __restrict__ grow = v.gGrow;
+  DP(const int32_t) r = v.iR + (one ? 0 : par) * P.I;
+  DPN(int32_t) bmin = one ? v.iR + P.I : v.iBmin + par * P.I;
+  DPN(int32_t) gang = v.fGang + par * P.F;
+  DP(const int32_t) grow = v.gGrow;
   // row sizes as of the last repack: in overlapped slots warp 0 appends (cold) residents
   // beyond them while this runs; rows below gNs never move (commit)
-  const int32_t* __restrict__ gn = v.gNs;
-  const int32_t* __restrict__ gres = v.gRes;
-  const int32_t* __restrict__ meta_ = v.iMeta;
-  const int32_t* __restrict__ ready = v.iReady;
-  const int32_t* __restrict__ ifunc = v.iFunc;
-  const int32_t* __restrict__ iid = v.iId;
-  const int32_t* __restrict__ fkind = v.fKind;
-  const int32_t* __restrict__ freq = v.fReq;
-  const int32_t* __restrict__ flim = v.fLim;
-  const int32_t* __restrict__ fdtr = v.fDtr;
-  const int32_t* __restrict__ fibs = v.fIbs;
-  const int32_t* __restrict__ fcb = v.fCb;
-  const int32_t* __restrict__ cbase = v.h + H_CBASE;
-  const int32_t* __restrict__ ccnt = v.h + H_CCNT;
-  const int32_t* __restrict__ gbase = v.h + H_GBASE;
+  DP(const int32_t) gn = v.gNs;
+  DP(const int32_t) gres = v.gRes;
+  DP(const int32_t) meta_ = v.iMeta;
+  DP(const int32_t) ready = v.iReady;
+  DP(const int32_t) ifunc = v.iFunc;
+  DP(const int32_t) iid = v.iId;
+  DP(const int32_t) fkind = v.fKind;
+  DP(const int32_t) freq = v.fReq;
+  DP(const int32_t) flim = v.fLim;
+  DP(const int32_t) fdtr = v.fDtr;
+  DP(const int32_t) fibs = v.fIbs;
+  DP(const int32_t) fcb = v.fCb;
+  DP(const int32_t) cbase = v.h + H_CBASE;
+  DP(const int32_t) ccnt = v.h + H_CCNT;
+  DP(const int32_t) gbase = v.h + H_GBASE;
   const int32_t nch = cbase[6];
   const int32_t T = (int32_t)P.T_slot, slot_ms = P.slot_ms;
   const uint64_t ht = sm64(sm64((uint32_t)c.scn_id) ^ (uint32_t)t);   // mix() prefix, per slot
@@ -1127,14 +1148,14 @@ static __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
   const Params& P = *c.P;
   const int par = t & 1;
   const bool one = P.SPS == 1;          // buffers as in phase1
-  const int32_t* __restrict__ r = v.iR + (one ? 0 : par) * P.I;
-  int32_t* bmin = one ? v.iR + P.I : v.iBmin + par * P.I;
-  int32_t* gang = v.fGang + par * P.F;
-  const int32_t* __restrict__ defl = v.fDefL;
-  const int32_t* __restrict__ reg = v.fReg;
-  const int32_t* __restrict__ lh = v.fLh;
-  const int32_t* __restrict__ nxt = v.iNext;
-  const int32_t* __restrict__ meta = v.iMeta;
+  DP(const int32_t) r = v.iR + (one ? 0 : par) * P.I;
+  DPN(int32_t) bmin = one ? v.iR + P.I : v.iBmin + par * P.I;
+  DPN(int32_t) gang = v.fGang + par * P.F;
+  DP(const int32_t) defl = v.fDefL;
+  DP(const int32_t) reg = v.fReg;
+  DP(const int32_t) lh = v.fLh;
+  DP(const int32_t) nxt = v.iNext;
+  DP(const int32_t) meta = v.iMeta;
   const int32_t ndef = v.h[H_NDEF];
   for (int32_t k = c.g.rank(); k < ndef; k += c.g.size()) {
     const int32_t f = defl[k];
@@ -1197,14 +1218,14 @@ template <bool LAT>
 static __device__ void phase0_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
-  const int32_t* __restrict__ infl = v.fInfL;
-  const int32_t* __restrict__ reg = v.fReg;
-  int32_t* __restrict__ pidx = v.fPidx;
-  const int32_t* __restrict__ lh = v.fLh;
-  const int32_t* __restrict__ nxt = v.iNext;
-  const int32_t* __restrict__ meta = v.iMeta;
-  const int32_t* __restrict__ ready = v.iReady;
-  int32_t* __restrict__ rb = v.rB;
+  DP(const int32_t) infl = v.fInfL;
+  DP(const int32_t) reg = v.fReg;
+  DP(int32_t) pidx = v.fPidx;
+  DP(const int32_t) lh = v.fLh;
+  DP(const int32_t) nxt = v.iNext;
+  DP(const int32_t) meta = v.iMeta;
+  DP(const int32_t) ready = v.iReady;
+  DP(int32_t) rb = v.rB;
   const int32_t Tp = P.Tp, ninf = v.h[H_NINF], I = P.I;
   for (int32_t k = c.g.rank(); k < ninf; k += c.g.size()) {
     const int32_t f = infl[k];
@@ -1242,7 +1263,7 @@ static __device__ void phase0_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
       }
       const int32_t q = A / nw, rem = A - q * nw;
       int32_t rank = 0;
-      int32_t* __restrict__ ru = rb + (size_t)u * I;
+      DP(int32_t) ru = rb + (size_t)u * I;
       for (int32_t s = s0; s >= 0; s = nxt[s]) {
         if (st_of(meta[s]) == ST_PLACED && ready[s] <= tu) {
           ru[s] = q + (rank < rem ? 1 : 0);
@@ -1260,9 +1281,9 @@ static __device__ void phase1_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
-  const int32_t* __restrict__ cbase = v.h + H_CBASE;
-  const int32_t* __restrict__ ccnt = v.h + H_CCNT;
-  const int32_t* __restrict__ gbase = v.h + H_GBASE;
+  DP(const int32_t) cbase = v.h + H_CBASE;
+  DP(const int32_t) ccnt = v.h + H_CCNT;
+  DP(const int32_t) gbase = v.h + H_GBASE;
   const int32_t nch = cbase[6];
   const int32_t T = (int32_t)P.T_slot, slot_ms = P.slot_ms, I = P.I, F = P.F;
   const uint64_t hs = sm64((uint32_t)c.scn_id);
@@ -1362,10 +1383,10 @@ template <bool LAT>
 static __device__ void phase2_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
-  const int32_t* __restrict__ defl = v.fDefL;
-  const int32_t* __restrict__ lh = v.fLh;
-  const int32_t* __restrict__ nxt = v.iNext;
-  const int32_t* __restrict__ meta = v.iMeta;
+  DP(const int32_t) defl = v.fDefL;
+  DP(const int32_t) lh = v.fLh;
+  DP(const int32_t) nxt = v.iNext;
+  DP(const int32_t) meta = v.iMeta;
   const int32_t ndef = v.h[H_NDEF], I = P.I, F = P.F;
   for (int32_t k = c.g.rank(); k < ndef; k += c.g.size()) {
     const int32_t f = defl[k];
@@ -1434,16 +1455,16 @@ static __device__ __forceinline__ int32_t a2_grow(int32_t r_last) {   // ceil(ma
 }
 
 template <bool LAT>
-static __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, const int32_t* rbase, size_t rstride,
-                            int32_t* bminb, size_t bstride, int32_t* gangb, size_t gstride,
-                            int32_t* emaxb, Acc& acc) {
+static __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, DPN(const int32_t) rbase, size_t rstride,
+                            DPN(int32_t) bminb, size_t bstride, DPN(int32_t) gangb, size_t gstride,
+                            DPN(int32_t) emaxb, Acc& acc) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
   const unsigned FULL = 0xffffffffu;
-  const int32_t* __restrict__ cbase = v.h + H_CBASE;
-  const int32_t* __restrict__ ccnt = v.h + H_CCNT;
-  const int32_t* __restrict__ gbase = v.h + H_GBASE;
+  DP(const int32_t) cbase = v.h + H_CBASE;
+  DP(const int32_t) ccnt = v.h + H_CCNT;
+  DP(const int32_t) gbase = v.h + H_GBASE;
   const int32_t nch = cbase[6];
   const int32_t NP = P.slot_ms / A2_PERIOD_MS;
   const long long PT = (long long)A2_PERIOD_MS * 1000;          // period in us
@@ -1648,20 +1669,20 @@ static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
   const int32_t sec = t / P.SPS;
   // B1 (function-parallel): window push, incremental counts, decisions, event flags.
   // Contiguous function ranges per thread keep the event list in ascending order.
-  const int32_t* __restrict__ fkind = v.fKind;
-  int32_t* __restrict__ reg = v.fReg;
-  const int32_t* __restrict__ farr = v.fArr;
-  const int32_t* __restrict__ fdep = v.fDep;
-  const long long* __restrict__ fcap1 = reinterpret_cast<const long long*>(v.fCap1);
-  int32_t* __restrict__ facc = v.fAcc;
-  int32_t* __restrict__ fhead = v.fHead;
-  int32_t* __restrict__ fns = v.fNsamp;
-  int32_t* __restrict__ fthr = v.fThrn;
-  int32_t* __restrict__ fup = v.fUp;
-  int32_t* __restrict__ fdown = v.fDown;
-  const int32_t* __restrict__ fnlive = v.fNlive;
-  int32_t* __restrict__ fflag = v.fFlag;
-  int32_t* __restrict__ ringb = v.ring;
+  DP(const int32_t) fkind = v.fKind;
+  DP(int32_t) reg = v.fReg;
+  DP(const int32_t) farr = v.fArr;
+  DP(const int32_t) fdep = v.fDep;
+  DP(const int64_t) fcap1 = v.fCap1;
+  DP(int32_t) facc = v.fAcc;
+  DP(int32_t) fhead = v.fHead;
+  DP(int32_t) fns = v.fNsamp;
+  DP(int32_t) fthr = v.fThrn;
+  DP(int32_t) fup = v.fUp;
+  DP(int32_t) fdown = v.fDown;
+  DP(const int32_t) fnlive = v.fNlive;
+  DP(int32_t) fflag = v.fFlag;
+  DP(int32_t) ringb = v.ring;
   const int32_t W = P.W;
   const int32_t per = (P.F + c.g.size() - 1) / c.g.size();
   const int32_t lo = c.g.rank() * per, hi = min(P.F, lo + per);
@@ -1675,7 +1696,7 @@ static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
     if (kind != K_UNUSED) {
       if (reg[f]) {
         const bool inf = is_inf(kind);
-        int32_t* ring = ringb + (size_t)f * W;
+        DPN(int32_t) ring = ringb + (size_t)f * W;
         const long long cap1 = fcap1[f];
         int32_t last = 0;
         if (inf && sec >= 1) {                      // step 1: push second sec-1
@@ -1742,6 +1763,9 @@ static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
     fflag[f] = ev;
     cnt += ev != 0;
   }
+#ifdef DILU_PHASE_TIMING
+  const long long cb0 = clock64();   // st[22]: B1 count barrier -> end of compaction (leader)
+#endif
   const int32_t any = g_count(c, cnt);
   int32_t total = 0;
   if (any) {                                        // ordered compaction of the events
@@ -1750,6 +1774,9 @@ static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
       if (fflag[f]) { v.fList[pos++] = f; --cnt; }
     c.g.sync();                                     // the event list is complete before B3
   }
+#ifdef DILU_PHASE_TIMING
+  if (c.g.leader()) acc.z->st[22] += clock64() - cb0;
+#endif
   const int32_t need_pass = total > 0 || v.h[H_QLEN] > 0;   // uniform: QLEN only changes in B3/placement
 #ifdef DILU_PHASE_TIMING
   long long bt0 = clock64();
@@ -1829,7 +1856,11 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
   }
   if (threadIdx.x == 0) {
     sv = make_view(hot, gblock, P.L);
+#ifdef DILU_BOUNDS
+    sv.ring = Chk<int32_t>(P.ring + (size_t)sc * P.F * P.W, (long long)P.F * P.W, sv.ring.id);
+#else
     sv.ring = P.ring + (size_t)sc * P.F * P.W;
+#endif
   }
   Scn c{sv};
   c.P = &P;
@@ -1839,13 +1870,13 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
   c.g.off = 0;
   c.g.gu = P.gscratch + (size_t)sc * GSCR;
   c.g.gi = reinterpret_cast<int32_t*>(c.g.gu + 32);
-  if (K == 1) {
-    c.members = red.members;
-    c.flag = red.flag;
-  } else {
-    c.members = reinterpret_cast<int32_t*>(c.g.gu + 48);
-    c.flag = reinterpret_cast<int32_t*>(c.g.gu + 80);
-  }
+  int32_t* const mem = K == 1 ? red.members : reinterpret_cast<int32_t*>(c.g.gu + 48);
+#ifdef DILU_BOUNDS
+  c.members = Chk<int32_t>(mem, 64, DILU_ID_MEMBERS);
+#else
+  c.members = mem;
+#endif
+  c.flag = K == 1 ? red.flag : reinterpret_cast<int32_t*>(c.g.gu + 80);
   c.frow = P.funcs + (size_t)sc * P.F * 16;
   c.scn_id = P.scen[sc * 4 + 0];
   c.om = P.scen[sc * 4 + 1];
@@ -1931,11 +1962,21 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
           Scn cw = c;
           cw.g.off = 32;
           const int nb = (int)blockDim.x - 32;
+#ifdef DILU_PHASE_TIMING
+          long long w0 = clock64(), w1;   // worker arm, first worker thread: st[19..21]
+#define WTICK(k) do { w1 = clock64(); if (threadIdx.x == 32) acc.z->st[k] += w1 - w0; w0 = w1; } while (0)
+#else
+#define WTICK(k) do { } while (0)
+#endif
           phase0<false>(cw, t, acc);
           asm volatile("bar.sync 1, %0;" :: "r"(nb) : "memory");
+          WTICK(19);
           phase1<false>(cw, t, acc);
           asm volatile("bar.sync 1, %0;" :: "r"(nb) : "memory");
+          WTICK(20);
           phase2<false>(cw, t, acc);
+          WTICK(21);
+#undef WTICK
         }
         __syncthreads();     // join: B1(t+1) resets the window fields P0(t) accumulates
         TICK(4);
@@ -2127,6 +2168,8 @@ __global__ void k_init(Params P) {
   uint8_t* b = P.state + (size_t)sc * P.L.bytes;
   View v = make_view(b, b, P.L);
   const int32_t* rows = P.funcs + (size_t)sc * P.F * 16;
+  // (dilu_sim_reset zeroes the whole state area first: alignment gaps are defined bytes
+  // when the run kernel stages the hot region -- compute-sanitizer initcheck clean)
   for (int k = threadIdx.x; k < H_WORDS; k += blockDim.x) v.h[k] = 0;
   __syncthreads();
   if (threadIdx.x == 0) { v.h[H_FSTOP] = P.I; v.h[H_DIRTY] = 1; v.h[H_LASTEP] = -1; v.h[H_QNEWPOS] = -1; }

@@ -43,6 +43,7 @@ enum : int {
 
 struct Layout {
   int32_t G, F, I, W, B;   // B: slots per fused batch between second boundaries (1 = unfused)
+  int32_t A2, LT;          // literal Alg.2 / request-level latency arrays present
   // byte offsets inside one block
   size_t hdr;
   size_t gR, gL, gU, gN, gNs, gRes, gExcl, gGrow, gMask, gRel, rlG, rlE;
@@ -63,7 +64,7 @@ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B = 1,
                           bool alg2 = false, bool lat = false) {
   Layout L;
-  L.G = G; L.F = F; L.I = I; L.W = W; L.B = B;
+  L.G = G; L.F = F; L.I = I; L.W = W; L.B = B; L.A2 = alg2; L.LT = lat;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t at = o; o = align16(o + bytes); return at; };
   // hot region: touched every slot -> staged in shared memory when it fits
@@ -77,6 +78,9 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B 
   L.rlG = take(4 * RLOG); L.rlE = take(4 * RLOG);
   L.iId = take(4 * (size_t)I); L.iFunc = take(4 * (size_t)I); L.iMeta = take(4 * (size_t)I);
   L.iReady = take(4 * (size_t)I); L.iNext = take(4 * (size_t)I); L.iR = take(4 * 2 * (size_t)I);
+#ifdef DILU_HOT_PAD
+  take(DILU_HOT_PAD);                   // layout-sensitivity parity variant
+#endif
   L.fKind = take(4 * (size_t)F); L.fReq = take(4 * (size_t)F); L.fLim = take(4 * (size_t)F);
   L.fMem = take(4 * (size_t)F); L.fCb = take(4 * (size_t)F); L.fIbs = take(4 * (size_t)F);
   L.fNw = take(4 * (size_t)F); L.fCls = take(4 * (size_t)F); L.fDtr = take(4 * (size_t)F);
@@ -121,23 +125,58 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B 
   return L;
 }
 
+
+// ---- element pointers of the view ----------------------------------------------------
+// Normal builds: raw pointers.  -DDILU_BOUNDS (debug side library): every
+// array of the view is a checked pointer {base, offset, length, array id}; an index
+// outside [0, length) of its array prints the array, the index and the thread and traps.
+// Phase code declares its local aliases through DP()/DPN() so they stay checked too.
+#ifdef DILU_BOUNDS
+#ifdef __CUDACC__
+static __device__ __noinline__ void dilu_oob(int id, long long j, long long n);
+#endif
+template <class T> struct Chk {
+  T* b; long long o, n; int id;
+  __host__ __device__ Chk() : b(nullptr), o(0), n(0), id(-1) {}
+  __host__ __device__ Chk(T* b_, long long n_, int id_) : b(b_), o(0), n(n_), id(id_) {}
+  template <class U> __host__ __device__ Chk(const Chk<U>& x) : b(x.b), o(x.o), n(x.n), id(x.id) {}
+#ifdef __CUDACC__
+  template <class Ix> __device__ __forceinline__ T& operator[](Ix i) const {
+    const long long j = o + (long long)i;
+    if (j < 0 || j >= n) dilu_oob(id, j, n);
+    return b[j];
+  }
+#endif
+  template <class Ix> __host__ __device__ Chk operator+(Ix k) const { Chk r = *this; r.o += (long long)k; return r; }
+  __host__ __device__ operator T*() const { return b + o; }
+};
+#define VP(T) ::dilu::Chk<T>
+#define DP(T) ::dilu::Chk<T>
+#define DPN(T) ::dilu::Chk<T>
+#else
+#define VP(T) T*
+#define DP(T) T* __restrict__
+#define DPN(T) T*
+#endif
+
 // Typed view of one scenario's block (pointers into smem or global).
 struct View {
-  int32_t* h;
-  int32_t *gR, *gL, *gU, *gN, *gNs, *gRes, *gExcl, *gGrow, *gRel, *rlG, *rlE;
-  unsigned long long* gMask;
-  int32_t *iId, *iFunc, *iMeta, *iReady, *iSh0, *iShare, *iNext, *iR, *iBmin, *fstack;
-  int16_t* iG;
-  int32_t *fKind, *fPrio, *fReq, *fLim, *fMem, *fCb, *fIbs, *fNw, *fCold, *fCls, *fDtr, *fPat,
-      *fScale, *fPhase;
-  int64_t* fCap1;
-  int32_t *fReg, *fNsamp, *fAcc, *fHead, *fUp, *fDown, *fThrn, *fOld, *fPv, *fNlive, *fLh, *fLt, *fGang,
-      *fFlag, *fK, *fList, *fArr, *fDep, *fPidx, *fInfL, *fDefL;
-  int32_t *qFunc, *qFirst, *qN, *qFail, *qSlot, *iQ;
-  int32_t *rB, *bB, *gB;
-  int32_t *aTc, *aTm, *aRl, *aLe, *aSt, *aOw, *aDt;
-  int32_t *fSlo, *iEmax, *eB;
-  int32_t* ring;  // global [F][W]
+  typedef VP(int32_t) PI;
+  PI h;
+  PI gR, gL, gU, gN, gNs, gRes, gExcl, gGrow, gRel, rlG, rlE;
+  VP(unsigned long long) gMask;
+  PI iId, iFunc, iMeta, iReady, iSh0, iShare, iNext, iR, iBmin, fstack;
+  VP(int16_t) iG;
+  PI fKind, fPrio, fReq, fLim, fMem, fCb, fIbs, fNw, fCold, fCls, fDtr, fPat,
+      fScale, fPhase;
+  VP(int64_t) fCap1;
+  PI fReg, fNsamp, fAcc, fHead, fUp, fDown, fThrn, fOld, fPv, fNlive, fLh, fLt, fGang,
+      fFlag, fK, fList, fArr, fDep, fPidx, fInfL, fDefL;
+  PI qFunc, qFirst, qN, qFail, qSlot, iQ;
+  PI rB, bB, gB;
+  PI aTc, aTm, aRl, aLe, aSt, aOw, aDt;
+  PI fSlo, iEmax, eB;
+  PI ring;  // global [F][W]
 };
 
 #ifdef __CUDACC__
@@ -146,26 +185,64 @@ __host__ __device__
 inline View make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
   // arrays in the hot region resolve against `hot` (smem copy or b), the rest against b
   View v;
-#define P32(name) v.name = reinterpret_cast<int32_t*>((L.name < L.hot_bytes ? hot : b) + L.name)
+  const long long G = L.G, F = L.F, I = L.I, BB = L.B > 1 ? L.B : 0;
+  const long long AI = L.A2 ? I * MAXST : 0, AG = L.A2 ? G : 0;
+#ifdef DILU_BOUNDS
+  int id = 0;
+#define PT(T, name, cnt) v.name = Chk<T>(reinterpret_cast<T*>((L.name < L.hot_bytes ? hot : b) + L.name), (cnt), id++)
+#else
+#define PT(T, name, cnt) v.name = reinterpret_cast<T*>((L.name < L.hot_bytes ? hot : b) + L.name)
+#endif
+  // (order = DILU_ARRAY_NAMES below)
+#ifdef DILU_BOUNDS
+  v.h = Chk<int32_t>(reinterpret_cast<int32_t*>(hot + L.hdr), H_WORDS, id++);
+#else
   v.h = reinterpret_cast<int32_t*>(hot + L.hdr);
-  P32(gR); P32(gL); P32(gU); P32(gN); P32(gNs); P32(gRes); P32(gExcl); P32(gGrow); P32(gRel); P32(rlG); P32(rlE);
-  v.gMask = reinterpret_cast<unsigned long long*>((L.gMask < L.hot_bytes ? hot : b) + L.gMask);
-  P32(iId); P32(iFunc); P32(iMeta); P32(iReady); P32(iSh0); P32(iShare); P32(iNext); P32(iR);
-  v.iG = reinterpret_cast<int16_t*>((L.iG < L.hot_bytes ? hot : b) + L.iG);
-  P32(iBmin); P32(fstack);
-  P32(fKind); P32(fPrio); P32(fReq); P32(fLim); P32(fMem); P32(fCb); P32(fIbs); P32(fNw);
-  P32(fCold); P32(fCls); P32(fDtr); P32(fPat); P32(fScale); P32(fPhase);
-  v.fCap1 = reinterpret_cast<int64_t*>(hot + L.fCap1);
-  P32(fReg); P32(fNsamp); P32(fAcc); P32(fHead); P32(fUp); P32(fDown); P32(fThrn); P32(fOld); P32(fPv); P32(fNlive);
-  P32(fLh); P32(fLt); P32(fGang); P32(fFlag); P32(fK); P32(fList); P32(fArr); P32(fDep);
-  P32(fPidx); P32(fInfL); P32(fDefL);
-  P32(qFunc); P32(qFirst); P32(qN); P32(qFail); P32(qSlot); P32(iQ);
-  P32(rB); P32(bB); P32(gB);
-  P32(aTc); P32(aTm); P32(aRl); P32(aLe); P32(aSt); P32(aOw); P32(aDt);
-  P32(fSlo); P32(iEmax); P32(eB);
-#undef P32
+#endif
+  PT(int32_t, gR, G); PT(int32_t, gL, G); PT(int32_t, gU, G); PT(int32_t, gN, G); PT(int32_t, gNs, G);
+  PT(int32_t, gRes, G * RES); PT(int32_t, gExcl, G); PT(int32_t, gGrow, G); PT(int32_t, gRel, G);
+  PT(int32_t, rlG, RLOG); PT(int32_t, rlE, RLOG);
+  PT(unsigned long long, gMask, G);
+  PT(int32_t, iId, I); PT(int32_t, iFunc, I); PT(int32_t, iMeta, I); PT(int32_t, iReady, I);
+  PT(int32_t, iSh0, I); PT(int32_t, iShare, I * MAXST); PT(int32_t, iNext, I); PT(int32_t, iR, 2 * I);
+  PT(int32_t, iBmin, 2 * I); PT(int32_t, fstack, I);
+  PT(int16_t, iG, I * MAXST);
+  PT(int32_t, fKind, F); PT(int32_t, fPrio, F); PT(int32_t, fReq, F); PT(int32_t, fLim, F);
+  PT(int32_t, fMem, F); PT(int32_t, fCb, F); PT(int32_t, fIbs, F); PT(int32_t, fNw, F);
+  PT(int32_t, fCold, F); PT(int32_t, fCls, F); PT(int32_t, fDtr, F); PT(int32_t, fPat, F);
+  PT(int32_t, fScale, F); PT(int32_t, fPhase, F);
+  PT(int64_t, fCap1, F);
+  PT(int32_t, fReg, F); PT(int32_t, fNsamp, F); PT(int32_t, fAcc, F); PT(int32_t, fHead, F);
+  PT(int32_t, fUp, F); PT(int32_t, fDown, F); PT(int32_t, fThrn, F); PT(int32_t, fOld, F);
+  PT(int32_t, fPv, F); PT(int32_t, fNlive, F); PT(int32_t, fLh, F); PT(int32_t, fLt, F);
+  PT(int32_t, fGang, 2 * F); PT(int32_t, fFlag, F); PT(int32_t, fK, F); PT(int32_t, fList, F);
+  PT(int32_t, fArr, F); PT(int32_t, fDep, F); PT(int32_t, fPidx, F); PT(int32_t, fInfL, F);
+  PT(int32_t, fDefL, F);
+  PT(int32_t, qFunc, I); PT(int32_t, qFirst, I); PT(int32_t, qN, I); PT(int32_t, qFail, I);
+  PT(int32_t, qSlot, I); PT(int32_t, iQ, I);
+  PT(int32_t, rB, BB * I); PT(int32_t, bB, BB * I); PT(int32_t, gB, BB * F);
+  PT(int32_t, aTc, AI); PT(int32_t, aTm, AI); PT(int32_t, aRl, AI); PT(int32_t, aLe, AI);
+  PT(int32_t, aSt, AG); PT(int32_t, aOw, AG); PT(int32_t, aDt, AG);
+  PT(int32_t, fSlo, L.LT ? F : 0); PT(int32_t, iEmax, L.LT ? 2 * I : 0);
+  PT(int32_t, eB, L.LT ? BB * I : 0);
+#undef PT
+#ifdef DILU_BOUNDS
+  v.ring = Chk<int32_t>(nullptr, 0, id);   // set by the kernel (ring)
+#else
   v.ring = nullptr;
+#endif
+  (void)G; (void)F; (void)I; (void)BB; (void)AI; (void)AG;
   return v;
 }
+
+#define DILU_ARRAY_NAMES                                                                     \
+  "h", "gR", "gL", "gU", "gN", "gNs", "gRes", "gExcl", "gGrow", "gRel", "rlG", "rlE", "gMask", \
+  "iId", "iFunc", "iMeta", "iReady", "iSh0", "iShare", "iNext", "iR", "iBmin", "fstack", "iG",  \
+  "fKind", "fPrio", "fReq", "fLim", "fMem", "fCb", "fIbs", "fNw", "fCold", "fCls", "fDtr",     \
+  "fPat", "fScale", "fPhase", "fCap1", "fReg", "fNsamp", "fAcc", "fHead", "fUp", "fDown",      \
+  "fThrn", "fOld", "fPv", "fNlive", "fLh", "fLt", "fGang", "fFlag", "fK", "fList", "fArr",     \
+  "fDep", "fPidx", "fInfL", "fDefL", "qFunc", "qFirst", "qN", "qFail", "qSlot", "iQ", "rB",    \
+  "bB", "gB", "aTc", "aTm", "aRl", "aLe", "aSt", "aOw", "aDt", "fSlo", "iEmax", "eB", "ring",  \
+  "members"
 
 }  // namespace dilu

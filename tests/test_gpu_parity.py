@@ -94,11 +94,10 @@ def test_c4_sample_full_hour():
     run_pair(wl, [3600], snap=False)
 
 
-@pytest.mark.parametrize("mode", ["cta_threads64", "cta_threads1024", "cta_no_smem", "cta_no_ovl", "lanes_p4",
-                                  "lanes_p16", "lanes_p8"])
+@pytest.mark.parametrize("mode", ["cta_threads64", "cta_threads1024", "cta_no_smem", "cta_no_ovl",
+                                  "cluster_k1", "cluster_k3"])
 def test_launch_shape_invariance(mode, monkeypatch):
-    """Both engines and several launch shapes give bit-identical results (45 scenarios:
-    a partial 32-scenario group for the lanes engine)."""
+    """Both engines and several launch shapes give bit-identical results (45 scenarios)."""
     full = di.c4(n_scenarios=4096, T=600)
     wl = full.subset(np.arange(5, 4096, 91))
     engine, _, shape = mode.partition("_")
@@ -111,12 +110,12 @@ def test_launch_shape_invariance(mode, monkeypatch):
         monkeypatch.setenv("DILU_NO_SMEM", "1")
     elif shape == "no_ovl":          # placement pass not overlapped with P0/P1/P2
         monkeypatch.setenv("DILU_NO_OVL", "1")
-    elif shape.startswith("p"):
-        monkeypatch.setenv("DILU_PARTS", shape[1:])
+    elif shape.startswith("k"):
+        monkeypatch.setenv("DILU_CLUSTER", shape[1:])
     run_pair(wl, [1, 599], id_cap=2048)
 
 
-@pytest.mark.parametrize("engine", ["cta", "lanes", "cluster"])
+@pytest.mark.parametrize("engine", ["cta", "cluster"])
 def test_engines_on_c1_c2(engine, monkeypatch):
     monkeypatch.setenv("DILU_ENGINE", engine)
     run_pair(di.c1(), [1, 39, 1, 59], id_cap=16)
@@ -230,7 +229,7 @@ def test_baseline_mode_c2(mode):
     run_pair(wl, [1, 299, 600], id_cap=4096)
 
 
-@pytest.mark.parametrize("engine", ["cta", "lanes", "cluster"])
+@pytest.mark.parametrize("engine", ["cta", "cluster"])
 def test_mixed_modes_c4_slice(engine, monkeypatch):
     """40 C4 sweep points, scenario i under mode i % 5, every engine."""
     monkeypatch.setenv("DILU_ENGINE", engine)

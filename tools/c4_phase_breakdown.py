@@ -19,7 +19,7 @@ per = np.zeros((n, 24), dtype=np.int64)
 lib().dilu_kernel_stats(sim.h, per.ctypes.data, None)
 names = ["attempts", "retry_checks", "row_repacks", "boundary_events", "queue_scans", "slots",
          "resident_slots", "function_slots", "pre_boundary", "boundary", "repack", "p0", "p1", "p2",
-         "b3", "terminate", "enqueue", "next_attempt", "place", "t19", "t20", "t21", "t22", "t23"]
+         "b3", "terminate", "enqueue", "next_attempt", "place", "w_p0", "w_p1", "w_p2", "b1_count_scan", "t23"]
 tot = per.sum(0)
 ss = tot[5]
 out = {"ms": s0.elapsed_time(s1), "scenario_slots": int(ss)}
