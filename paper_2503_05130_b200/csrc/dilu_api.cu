@@ -12,6 +12,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "../../include/dilu.h"
 #include "sim_kernel.cuh"
@@ -36,6 +37,7 @@ struct dilu_sim {
   int32_t status;
   bool use_smem;
   int threads;
+  std::vector<int8_t> kind;   // host copy of every function row's kind (place_batch validation)
   char err[512];
 };
 
@@ -286,6 +288,8 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   *out = s;
 
   const size_t S = cfg->n_scenarios, F = cfg->max_funcs;
+  try { s->kind.resize(S * F); } catch (...) { return fail(s, DILU_E_USAGE, "out of host memory"); }
+  for (size_t i = 0; i < S * F; ++i) s->kind[i] = (int8_t)h_funcs[i].kind;
   // H->D copies of the inputs (caller's stream)
   dilu_status rc;
   if ((rc = cuda_check(s, cudaMemcpyAsync(s->ws + k.funcs, h_funcs, S * F * sizeof(dilu_func),
@@ -444,25 +448,23 @@ dilu_status dilu_place_batch(dilu_sim* s, int32_t n_req, const int32_t* d_req_sc
   if (s->status) return DILU_E_STATE;
   if (n_req < 0 || (n_req > 0 && (!d_req_scenario || !d_req_func || !d_out_gpu || !d_out_iid)))
     return fail(s, DILU_E_USAGE, "place_batch: bad request arrays");
-  // request validation needs the function table: done on the host copy of the requests
+  // request validation against the host copy of the function kinds kept at create: one
+  // bulk copy of the two request arrays, one stream sync, no per-request round trips
   if (n_req > 0) {
-    int32_t* hs = new (std::nothrow) int32_t[2 * (size_t)n_req];
-    if (!hs) return fail(s, DILU_E_USAGE, "out of host memory");
-    cudaError_t e1 = cudaMemcpyAsync(hs, d_req_scenario, 4 * (size_t)n_req, cudaMemcpyDeviceToHost, s->stream);
-    cudaError_t e2 = cudaMemcpyAsync(hs + n_req, d_req_func, 4 * (size_t)n_req, cudaMemcpyDeviceToHost, s->stream);
-    cudaError_t e3 = cudaStreamSynchronize(s->stream);
-    if (e1 || e2 || e3) { delete[] hs; return cuda_check(s, e1 ? e1 : (e2 ? e2 : e3), "place_batch copy"); }
-    dilu_func fr;
+    std::vector<int32_t> hs;
+    try { hs.resize(2 * (size_t)n_req); } catch (...) { return fail(s, DILU_E_USAGE, "out of host memory"); }
+    dilu_status rc = cuda_check(s, cudaMemcpyAsync(hs.data(), d_req_scenario, 4 * (size_t)n_req,
+                                                   cudaMemcpyDeviceToHost, s->stream), "place_batch copy");
+    if (!rc) rc = cuda_check(s, cudaMemcpyAsync(hs.data() + n_req, d_req_func, 4 * (size_t)n_req,
+                                                cudaMemcpyDeviceToHost, s->stream), "place_batch copy");
+    if (!rc) rc = cuda_check(s, cudaStreamSynchronize(s->stream), "place_batch sync");
+    if (rc) return rc;
     for (int32_t j = 0; j < n_req; ++j) {
       const int32_t sc = hs[j], f = hs[n_req + j];
-      bool ok = sc >= 0 && sc < s->cfg.n_scenarios && f >= 0 && f < s->cfg.max_funcs;
-      if (ok) {
-        cudaMemcpy(&fr, s->P.funcs + ((size_t)sc * s->cfg.max_funcs + f) * 16, sizeof fr, cudaMemcpyDeviceToHost);
-        ok = fr.kind != K_UNUSED;
-      }
-      if (!ok) { delete[] hs; return fail(s, DILU_E_USAGE, "place_batch: request %d names an invalid scenario/function", j); }
+      const bool ok = sc >= 0 && sc < s->cfg.n_scenarios && f >= 0 && f < s->cfg.max_funcs &&
+                      s->kind[(size_t)sc * s->cfg.max_funcs + f] != K_UNUSED;
+      if (!ok) return fail(s, DILU_E_USAGE, "place_batch: request %d names an invalid scenario/function", j);
     }
-    delete[] hs;
   }
   return launch_run(s, 0, n_req, d_req_scenario, d_req_func, d_out_gpu, d_out_iid);
 }

@@ -27,15 +27,24 @@ def block(n: int, rank: int, world: int) -> Tuple[int, int]:
     return n * rank // world, n * (rank + 1) // world
 
 
-def init(backend: str = "nccl"):
-    """Initialise the default process group when launched with world_size > 1."""
+def init(backend: str = "nccl", device=None):
+    """Initialise the default process group when launched with world_size > 1.  With NCCL
+    the caller has already selected its GPU (torch.cuda.set_device) and passes it as
+    ``device`` (bound to the group: eager communicator init on the right device)."""
     import torch.distributed as dist
     rank, world, _ = env_rank()
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29511")
-        dist.init_process_group(backend=backend, rank=rank, world_size=world)
+        kw = {"device_id": device} if (backend == "nccl" and device is not None) else {}
+        dist.init_process_group(backend=backend, rank=rank, world_size=world, **kw)
     return rank, world
+
+
+def finalize():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.destroy_process_group()
 
 
 def allreduce_tallies(t, group=None):
@@ -43,7 +52,12 @@ def allreduce_tallies(t, group=None):
     uint64 hash field wraps identically under int64 two's-complement addition."""
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        if dist.get_backend(group) == "gloo" and t.is_cuda:   # gloo: host copy
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t
 
 

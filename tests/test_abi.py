@@ -106,3 +106,17 @@ def test_abi_argument_errors_without_gpu():
     assert pkg.dilu_workspace_bytes(cfg) > 0                     # 1 s slots: fine
     cfg[di.CONFIG_FIELDS.index("slot_ms")] = 8                   # not a multiple of 5
     assert pkg.dilu_workspace_bytes(cfg) == 0
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """bench.py --gpus N outside torchrun spawns N ranks itself, and refuses clearly (exit
+    2, message) when fewer than N GPUs are visible (a 1-GPU --gpus 2 run must
+    not silently time one GPU)."""
+    import subprocess, sys, os, torch
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    n = torch.cuda.device_count()
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", str(n + 1)],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 2
+    assert "visible GPUs" in r.stderr
