@@ -460,3 +460,17 @@ def test_c5_bench_shape_window():
     initial ~28k-instance fleet placement per scenario)."""
     wl = di.c5(n_scenarios=8, T=600, first_seed=50)
     run_pair(wl, [600], snap=False)
+
+
+def test_c5_timed_window_vs_frozen_oracle():
+    """C5 at the bench's full timed window (8 x 16,384 GPUs, 36,000 x 100 ms slots, the bench
+    launch shape) against the oracle's per-scenario tallies frozen by
+    tools/freeze_c5_golden.py (a committed script that calls only oracle/)."""
+    import json
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c5_window_tallies.json")))
+    wl = di.c5(n_scenarios=8, T=36000, first_seed=50)
+    gs = gpu_sim(wl)
+    gs.scale_step(36000)
+    per, tot = gs.metrics()
+    assert np.array_equal(per.cpu().numpy(), np.array(gold["per_scenario"], dtype=np.int64))
+    assert np.array_equal(tot.cpu().numpy(), np.array(gold["sum"], dtype=np.int64))
