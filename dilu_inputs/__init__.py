@@ -179,17 +179,85 @@ def profile_sessions(n: int, seed: int = 0) -> np.ndarray:
     return out
 
 
-# --------------------------------------------------------------- quantiser (a0)
+# ------------------------------------------------- catalogue rows for the a0 loader
 
-def quantise_profile(req_pct: float, lim_pct: float, mem_gb: float, cold_ms: float,
-                     slot_ms: int) -> Dict[str, int]:
-    """Loader rounding (Q25): req_pm = ceil(10*req%), lim_pm = min(1000, ceil(10*lim%)),
-    mem_mib = ceil(1024*GB), cold_slots = ceil(cold_ms/slot_ms).  Applied once."""
-    eps = 1e-9
-    return dict(req_pm=int(math.ceil(10 * req_pct - eps)),
-                lim_pm=min(1000, int(math.ceil(10 * lim_pct - eps))),
-                mem_mib=int(math.ceil(1024 * mem_gb - eps)),
-                cold_slots=int(math.ceil(cold_ms / slot_ms - eps)))
+# One catalogue row per function before quantisation (include/dilu.h dilu_catalog_row):
+# the profiled quotas come from the function's profiling session; memory (GB), cold start
+# (ms) and SLO (ms) are real-valued model facts.  Input data only: the quantisation (Q25,
+# R4) is the loader's (oracle/dilu_ref_load.c, csrc/profile.cuh k_load).
+CATALOG_ROW = np.dtype([("kind", "<i4"), ("prio", "<i4"), ("n_workers", "<i4"), ("duty_pm", "<i4"),
+                        ("affinity_class", "<i4"), ("arrive_sec", "<i4"), ("depart_sec", "<i4"),
+                        ("pattern", "<i4"), ("scale_q10", "<i4"), ("phase_slots", "<i4"),
+                        ("reserved", "<i4", (2,)), ("mem_gb", "<f8"), ("cold_ms", "<f8"),
+                        ("slo_ms", "<f8")])
+assert CATALOG_ROW.itemsize == 72
+
+
+def profiled_fleet(seed: int = 0, T: int = 900, n_inf: int = 120, n_llm: int = 40, n_train: int = 40):
+    """A C2-shaped fleet described before profiling (SURVEY s8(a) a0 input): per function
+    a profiling session (``PROF_SESSION``, the built-in latency / throughput models with
+    jitter) and a catalogue row (``CATALOG_ROW``: memory in GB, cold start in ms, SLO in ms,
+    lifecycle, arrival pattern).  Returns (sessions, catalogue, patterns); the loader turns
+    profiling results + catalogue into the function table (profile -> load -> simulate)."""
+    rng = _rng(seed, "catalog")
+    pats = make_patterns(T, 1000, 1300 + seed, diurnal=False)
+    pat_mean = pats.mean(axis=1)
+    n = n_inf + n_llm + n_train
+    ses = np.zeros(n, PROF_SESSION)
+    cat = np.zeros(n, CATALOG_ROW)
+    A = np.array([m[1:] for m in PROFILE_MODELS_V1])
+    Tr = np.array([m[1:] for m in PROFILE_TRAIN_V1])
+    for i in range(n):
+        j = lambda: rng.uniform(0.9, 1.1)
+        if i < n_inf + n_llm:
+            llm = i >= n_inf
+            mi = 3 if llm else int(rng.integers(0, 3))         # llama2-7b-like for LLMs
+            ses[i]["kind"], ses[i]["workers"], ses[i]["ibs_max"] = 0, 1, 32
+            ses[i]["a_ms"], ses[i]["b_ms"] = A[mi, 0] * j(), A[mi, 1] * j()
+            ses[i]["knee_c"], ses[i]["slo_ms"] = A[mi, 2] * j(), A[mi, 3]
+            ses[i]["smr_step"] = 10.0
+            pat = int(BURSTY_FAMILY[rng.integers(len(BURSTY_FAMILY))])
+            nominal_rps = 4 * 1000.0 / (A[mi, 3] / 2.0)          # a nominal IBS-4 server
+            u = rng.uniform(0.2, 0.8)
+            cat[i]["kind"] = K_LLM if llm else K_INF
+            cat[i]["prio"] = 0
+            cat[i]["n_workers"] = 1
+            cat[i]["mem_gb"] = rng.choice([14.0, 16.0]) if llm else rng.choice([1.0, 2.0, 4.0, 6.0, 1.5])
+            cat[i]["cold_ms"] = 10000.0 if llm else rng.choice([2000.0, 2500.0, 3000.0])
+            cat[i]["slo_ms"] = A[mi, 3]
+            cat[i]["pattern"] = pat
+            cat[i]["scale_q10"] = int(round(1024.0 * u * nominal_rps / max(pat_mean[pat], 1e-3)))
+            cat[i]["phase_slots"] = int(rng.integers(0, T))
+            cat[i]["affinity_class"] = int(cat[i]["kind"]) * 1000 + pat
+            cat[i]["arrive_sec"], cat[i]["depart_sec"] = 0, NEVER
+        else:
+            mi = int(rng.integers(0, 4))
+            w = int(rng.choice([1, 2, 4], p=[0.5, 0.3, 0.2]))
+            ses[i]["kind"], ses[i]["workers"] = 2, w
+            ses[i]["knee_t"] = min(100.0, Tr[mi, 0] * j())
+            ses[i]["t_max"], ses[i]["idle"] = Tr[mi, 1] * j(), min(0.6, Tr[mi, 2] * j())
+            ses[i]["p_req"], ses[i]["p_lim"], ses[i]["tol"] = 0.8, 1.0, 0.02
+            arr = int(rng.integers(0, T))
+            cat[i]["kind"], cat[i]["prio"], cat[i]["n_workers"] = K_TRAIN, 1, w
+            cat[i]["duty_pm"] = int(rng.integers(600, 1001))
+            cat[i]["mem_gb"] = rng.choice([8.0, 10.0, 12.0, 20.0])
+            cat[i]["cold_ms"] = 5000.0
+            cat[i]["pattern"] = -1
+            cat[i]["affinity_class"] = 2000 + i
+            cat[i]["arrive_sec"] = arr
+            cat[i]["depart_sec"] = arr + int(rng.integers(600, 2400))
+    return ses, cat, pats
+
+
+def workload_from_rows(name: str, rows: np.ndarray, patterns: np.ndarray, T: int,
+                       gpus: int = 64, max_instances: int = 512) -> Workload:
+    """One scenario over already-loaded function rows (int32 [F, 16])."""
+    funcs = np.ascontiguousarray(rows, dtype=np.int32)[None]
+    cfg = default_config(n_scenarios=1, gpus_per_scenario=gpus, max_funcs=funcs.shape[1],
+                         max_instances=max_instances, n_patterns=patterns.shape[0],
+                         pattern_len=patterns.shape[1])
+    scen = np.array([[0, 1000, 1500, 0]], dtype=np.int32)
+    return Workload(name, cfg, scen, funcs, patterns, T, "loaded from profiles")
 
 
 # ------------------------------------------------------- model catalogue (s8(d))

@@ -123,7 +123,10 @@ typedef struct dilu_sim dilu_sim;
 /* Bytes of device workspace a handle needs for cfg (0 if cfg is invalid). */
 size_t dilu_workspace_bytes(const dilu_config* cfg);
 
-/* Validate the inputs (first violation named in *out's last error, or on stderr if
+/* Create the simulated clusters: the synthetic counterpart of the paper's large-scale
+ * simulation setup (s4.1: a cluster of GPUs, DL instances of training / LLM
+ * inference / non-LLM inference types, one profile-table row per function).
+ * Validate the inputs (first violation named in *out's last error, or on stderr if
  * *out cannot be created), copy them H->D into the workspace on the stream, and
  * initialise every scenario at slot 0 (no function registered, all GPUs inactive).
  *   cfg      host, read during the call
@@ -150,11 +153,20 @@ dilu_status dilu_sim_reset(dilu_sim* s);
 dilu_status dilu_place_batch(dilu_sim* s, int32_t n_req, const int32_t* d_req_scenario,
                              const int32_t* d_req_func, int32_t* d_out_gpu, int32_t* d_out_iid);
 
-/* Advance all scenarios by n_slots slots (boundary work included); stream-ordered,
- * no host synchronisation. */
+/* Advance all scenarios by n_slots slots (boundary work included): per second the lazy
+ * horizontal scaler over the sliding window (s3.4.2) and Alg.1
+ * placement of the queue; per slot the token-based vertical scaling
+ * (Alg.2 slot reading, or the literal 5 ms periods with cfg.flags bit2) and
+ * the metric fold.  Stream-ordered, no host synchronisation.  Errors: DILU_E_USAGE for
+ * n_slots < 0, DILU_E_STATE after a failed call, DILU_E_CUDA on a launch error (deferred
+ * DILU_E_CAPACITY surfaces at dilu_metrics). */
 dilu_status dilu_scale_step(dilu_sim* s, int32_t n_slots);
 
-/* Reduce tallies: per-scenario int64 [n_scenarios][DILU_NT] (may be NULL) and the
+/* The paper's metrics as integer tallies (PAPER.md:1147 s4.1 "Metrics": SVR, CSC,
+ * throughput; P:1379 aggregate throughput = served work over occupied resources;
+ * P:1436 / Fig. 13 SM and memory fragments of the active GPUs): the ratios are
+ * formed on the host from these exact sums (SURVEY s8(c) "Final ratios").
+ * Reduce tallies: per-scenario int64 [n_scenarios][DILU_NT] (may be NULL) and the
  * scenario sum int64 [DILU_NT] (uint64 wrap-sum for the hash, may be NULL).  Pointers
  * may be host or device (copied with cudaMemcpyDefault).  Synchronises the stream and
  * returns any deferred DILU_E_CAPACITY / DILU_E_CUDA. */
@@ -228,6 +240,41 @@ typedef struct {
  * d_out[i].status, not call errors.  No handle needed. */
 dilu_status dilu_profile(const dilu_prof_session* d_sessions, int32_t n, dilu_prof_out* d_out,
                          void* cuda_stream);
+
+/* ---- profile-table loader: profiled tuples -> quantised rows --------
+ * PAPER.md s3.2 (Table 1 <IBS, request, limit, memory>; P:628 training
+ * request/limit at 80 % / 100 % of full throughput; P:634-637 inference request = the
+ * profiled SMR meeting SLO/2, limit = 2 x request).  One catalogue row per function plus
+ * the dilu_prof_out of its profiling session give one dilu_func row; readings Q25 and R4
+ * (DESIGN.md s3): req_pm / lim_pm are the session's Q25-rounded quotas, ibs the profiled
+ * IBS (inference), mem_mib = ceil(1024 * mem_gb), cold_slots = ceil(cold_ms / slot_ms),
+ * c_b = floor(req_pm * slo_ms / 2) tokens (R4; 0 for training), each ceil taken of the
+ * fp64 value minus 1e-9 (so exact decimal inputs are not pushed up by representation
+ * error).  The remaining fields are copied.  The rows then go to dilu_sim_create, which
+ * validates them (R1, R4, Q12, Q23, lifecycle). */
+typedef struct {
+  int32_t kind;            /* 0 inference, 1 LLM inference, 2 training                     */
+  int32_t prio;            /* 0 SLO-sensitive, 1 best-effort                               */
+  int32_t n_workers;       /* training: data-parallel workers; inference: ignored (1)     */
+  int32_t duty_pm;         /* training compute duty; inference: ignored            */
+  int32_t affinity_class, arrive_sec, depart_sec;
+  int32_t pattern, scale_q10, phase_slots;
+  int32_t reserved[2];     /* 0 */
+  double mem_gb;           /* memory footprint in GB (Table 1 "memory")                    */
+  double cold_ms;          /* cold-start latency in ms                                      */
+  double slo_ms;           /* inference SLO in ms; training: ignored                        */
+} dilu_catalog_row;        /* 72 bytes */
+
+/* Load n rows: d_cat[n] and d_prof[n] (the dilu_profile output of row i's session) in,
+ * d_out[n] rows and d_status[n] out, all device memory; stream-ordered and asynchronous.
+ * d_status[i]: 0 loaded; 1 the session's profile failed (status != 0) -> row written as
+ * unused (kind -1); 2 catalogue row invalid (kind out of range, kind and session disagree
+ * (inference vs training), non-finite or negative mem/cold/slo) -> unused.  Returns
+ * DILU_E_USAGE for n < 0, slot_ms outside 1..1000 or null pointers with n > 0,
+ * DILU_E_CUDA on a launch error. */
+dilu_status dilu_load_profiles(const dilu_catalog_row* d_cat, const dilu_prof_out* d_prof,
+                               int32_t n, int32_t slot_ms, dilu_func* d_out, int32_t* d_status,
+                               void* cuda_stream);
 
 #ifdef __cplusplus
 }

@@ -20,7 +20,7 @@ NT = 17
 
 
 def build(force: bool = False) -> str:
-    srcs = [os.path.join(_HERE, n) for n in ("dilu_ref.c", "dilu_ref_profile.c")]
+    srcs = [os.path.join(_HERE, n) for n in ("dilu_ref.c", "dilu_ref_profile.c", "dilu_ref_load.c")]
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
             [os.path.getmtime(x) for x in srcs] + [os.path.getmtime(os.path.join(_HERE, "dilu_ref.h"))]):
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-Wall", "-shared",
@@ -75,6 +75,8 @@ def lib():
         L.dilu_ref_lat_bucket.argtypes = [C.c_int64]
         L.dilu_ref_instance_latency.restype = None
         L.dilu_ref_instance_latency.argtypes = [C.c_int64] * 6 + [P64]
+        L.dilu_ref_load_batch.restype = None
+        L.dilu_ref_load_batch.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         L.dilu_ref_profile_batch.restype = None
         L.dilu_ref_profile_batch.argtypes = [C.c_int32, C.c_void_p, C.c_void_p]
         L.dilu_ref_infer_exec_ms.restype = C.c_double
@@ -238,3 +240,17 @@ def instance_latency(r, ibs, b, e, slo_us, T_us):
     lat = np.zeros(NLAT, dtype=np.int64)
     lib().dilu_ref_instance_latency(int(r), int(ibs), int(b), int(e), int(slo_us), int(T_us), lat)
     return lat
+
+
+def load_profiles(catalog, prof_out, slot_ms: int):
+    """The a0 loader oracle: ``dilu_inputs.CATALOG_ROW`` rows + ``PROF_OUT`` rows ->
+    (int32 [n, 16] function rows, int32 [n] status)."""
+    cat = np.ascontiguousarray(catalog)
+    pr = np.ascontiguousarray(prof_out)
+    n = len(cat)
+    assert len(pr) == n
+    rows = np.zeros((n, 16), dtype=np.int32)
+    st = np.zeros(n, dtype=np.int32)
+    lib().dilu_ref_load_batch(n, cat.ctypes.data, pr.ctypes.data, int(slot_ms), rows.ctypes.data,
+                              st.ctypes.data)
+    return rows, st

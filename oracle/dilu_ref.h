@@ -163,6 +163,21 @@ double dilu_ref_train_tput(const ref_prof_session* m, double smr);
 void dilu_ref_profile_one(const ref_prof_session* in, ref_prof_out* out);
 void dilu_ref_profile_batch(int32_t n, const ref_prof_session* in, ref_prof_out* out);
 
+/* ---- profile-table loader ----------
+ * dilu_ref_load.c.  One catalogue row + its profiling result -> one 16-int32 function row
+ * (field order of dilu_inputs.FUNC_FIELDS), readings Q25 and R4 of DESIGN.md s3. */
+typedef struct {
+  int32_t kind, prio, n_workers, duty_pm;
+  int32_t affinity_class, arrive_sec, depart_sec;
+  int32_t pattern, scale_q10, phase_slots;
+  int32_t reserved[2];
+  double mem_gb, cold_ms, slo_ms;
+} ref_catalog_row;
+int32_t dilu_ref_load_one(const ref_catalog_row* c, const ref_prof_out* p, int32_t slot_ms,
+                          int32_t* row16);
+void dilu_ref_load_batch(int32_t n, const ref_catalog_row* c, const ref_prof_out* p,
+                         int32_t slot_ms, int32_t* rows16, int32_t* status);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,9 @@ def lib():
         L.dilu_latency.argtypes = [vp, vp, vp]
         L.dilu_profile.restype = i32
         L.dilu_profile.argtypes = [vp, i32, vp, vp]
+        if hasattr(L, "dilu_load_profiles"):   # (older side libraries in A/B runs lack it)
+            L.dilu_load_profiles.restype = i32
+            L.dilu_load_profiles.argtypes = [vp, vp, i32, i32, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -71,7 +74,8 @@ def lib():
 EXPORTED = ["dilu_workspace_bytes", "dilu_sim_create", "dilu_sim_reset", "dilu_place_batch",
             "dilu_scale_step", "dilu_metrics", "dilu_snapshot", "dilu_kernel_stats",
             "dilu_current_slot",
-            "dilu_last_error", "dilu_sim_destroy", "dilu_profile", "dilu_latency"]
+            "dilu_last_error", "dilu_sim_destroy", "dilu_profile", "dilu_latency",
+            "dilu_load_profiles"]
 
 
 def _i32(a) -> np.ndarray:
@@ -225,6 +229,32 @@ def dilu_profile(sessions, out=None, stream=None):
     return out
 
 
+CATALOG_ROW_BYTES, FUNC_ROW_BYTES = 72, 64
+
+
+def dilu_load_profiles(catalog, prof_out, slot_ms: int, stream=None):
+    """Profile-table loader (dilu_load_profiles): ``catalog`` a uint8 CUDA
+    tensor of n * 72 bytes (dilu_catalog_row rows), ``prof_out`` the n * 48-byte
+    dilu_profile output of their sessions.  Returns (rows: int32 CUDA tensor [n, 16] =
+    dilu_func rows, status: int32 CUDA tensor [n]).  Asynchronous on ``stream``."""
+    import torch
+    for t, w in ((catalog, CATALOG_ROW_BYTES), (prof_out, PROF_OUT_BYTES)):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.uint8):
+            raise TypeError("catalog / prof_out must be uint8 CUDA tensors")
+    n = catalog.numel() // CATALOG_ROW_BYTES
+    if catalog.numel() != n * CATALOG_ROW_BYTES or prof_out.numel() != n * PROF_OUT_BYTES:
+        raise ValueError("catalog / prof_out sizes do not describe the same n rows")
+    rows = torch.empty((n, 16), dtype=torch.int32, device=catalog.device)
+    st = torch.empty(n, dtype=torch.int32, device=catalog.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(catalog.device)
+    rc = lib().dilu_load_profiles(catalog.data_ptr(), prof_out.data_ptr(), n, int(slot_ms),
+                                  rows.data_ptr(), st.data_ptr(), stream.cuda_stream)
+    if rc:
+        raise DiluError(rc, "dilu_load_profiles failed")
+    return rows, st
+
+
 def lat_bucket_bounds(b: int):
     """[lo, hi) in microseconds of latency bucket b (D10), hi = inf for 79."""
     if b >= 79:
@@ -247,11 +277,21 @@ def latency_summary(lat) -> dict:
            "latency_svr": float(lat[80]) / n if n else 0.0,
            "mean_ms": float(lat[81]) / served / 1000.0 if served else None}
     cum = np.cumsum(hist)
+    cum_s = np.cumsum(hist[:79])
     for q in (50, 95, 99):
+        # over all requests: an unserved request (capacity, bucket 79) has infinite latency,
+        # so the percentile is undefined (None) once more than (100 - q) % are unserved
         if n == 0:
             out[f"p{q}_ms"] = None
-            continue
-        b = int(np.searchsorted(cum, q / 100.0 * n, side="left"))
-        hi = lat_bucket_bounds(b)[1]
-        out[f"p{q}_ms"] = hi / 1000.0 if hi != float("inf") else None
+        else:
+            b = int(np.searchsorted(cum, q / 100.0 * n, side="left"))
+            hi = lat_bucket_bounds(b)[1]
+            out[f"p{q}_ms"] = hi / 1000.0 if hi != float("inf") else None
+        # over the served requests only (always defined when any request was served)
+        if served == 0:
+            out[f"p{q}_served_ms"] = None
+        else:
+            b = int(np.searchsorted(cum_s, q / 100.0 * served, side="left"))
+            out[f"p{q}_served_ms"] = lat_bucket_bounds(b)[1] / 1000.0
+    out["unserved_fraction"] = float(lat[79]) / n if n else 0.0
     return out

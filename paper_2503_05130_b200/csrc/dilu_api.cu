@@ -383,14 +383,51 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   const size_t static_smem = sizeof(Red) + sizeof(Params) + 64;
   s->use_smem = s->L.hot_bytes + static_smem <= (size_t)max_optin;
   const int32_t G = cfg->gpus_per_scenario;
+  // Narrow state (ET<true>) for the shared-memory kernels when the sizes allow
+  const bool nar = narrow_ok(G, cfg->max_funcs, cfg->max_instances, cfg->window_s);
+  const Layout Ln = make_layout(G, cfg->max_funcs, cfg->max_instances, cfg->window_s, choose_batch(cfg),
+                                (cfg->flags & 4) != 0, (cfg->flags & 8) != 0, true);
+  if (nar) s->use_smem = Ln.hot_bytes + static_smem <= (size_t)max_optin;
+  if (const char* e = getenv("DILU_NO_SMEM")) if (atoi(e)) s->use_smem = false;
   s->threads = G <= 256 && cfg->max_funcs <= 1024 ? 256 : (G <= 2048 ? 512 : 1024);
+  if (s->use_smem && nar) {
+    s->L = Ln;
+    P.L = Ln;
+  }
+  // Shared-memory kernels: the thread count that maximises resident scenarios per SM over
+  // per-scenario latency.  Latency per slot grows only slowly as threads shrink (C4:
+  // 454 / 457 / 478 / 495 / 511 ms at 256 / 224 / 192 / 160 / 128 threads and 3 CTAs/SM,
+  // DESIGN.md s7) while fewer threads and the narrow state let more scenarios share an SM.
+  if (s->use_smem && G <= 256) {
+    static const int cand[5] = {256, 224, 192, 160, 128};
+    static const double lat[5] = {454, 457, 478, 495, 511};
+    double best = 0.0;
+    for (int k = 0; k < 5; ++k) {
+      int per = 0;
+      if ((rc = cuda_check(s, cudaFuncSetAttribute(run_fn(true, variant_of(cfg, s->L)),
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)s->L.hot_bytes), "smem attribute")))
+        return rc;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, run_fn(true, variant_of(cfg, s->L)), cand[k],
+                                                        s->L.hot_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      const double score = per / lat[k];
+      if (score > best * 1.0001) { best = score; s->threads = cand[k]; }
+    }
+  }
   // test hooks: outputs must not depend on the launch shape
   if (const char* e = getenv("DILU_THREADS")) {
     const int v = atoi(e);
     if (v >= 32 && v <= 1024 && v % 32 == 0) s->threads = v;
   }
-  if (const char* e = getenv("DILU_NO_SMEM")) if (atoi(e)) s->use_smem = false;
   if (s->threads > SMEM_MAX_THREADS) s->use_smem = false;
+  if (!s->use_smem && s->L.N) {            // back to the wide state for the global kernels
+    s->L = make_layout(G, cfg->max_funcs, cfg->max_instances, cfg->window_s, choose_batch(cfg),
+                       (cfg->flags & 4) != 0, (cfg->flags & 8) != 0, false);
+    P.L = s->L;
+  }
   if (s->use_smem) {
     if ((rc = cuda_check(s, cudaFuncSetAttribute(run_fn(true, variant_of(cfg, s->L)),
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -419,6 +456,10 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
     const char* e = getenv("DILU_NO_OVL");
     P.ovl = cold_ok && variant_of(cfg, s->L) == 0 && G <= WARP_PLACE_MAX && s->threads >= 64 &&
             !(e && atoi(e));
+    // DILU_PIPE=1: the pipelined overlapped slot (B1 shares after P0, B3 split around the
+    // control arm) -- exact, measured slower on C4, kept as a parity variant
+    const char* pe = getenv("DILU_PIPE");
+    if (P.ovl && pe && atoi(pe)) P.ovl = 2;
   }
   if (getenv("DILU_VERBOSE"))
     fprintf(stderr, "dilu: cta engine threads=%d smem=%d hot=%zu per_sm=%d grid=%d ovl=%d\n", s->threads,
@@ -438,7 +479,8 @@ dilu_status dilu_sim_reset(dilu_sim* s) {
   dilu_status rc = cuda_check(s, cudaMemsetAsync(s->P.state, 0, (size_t)s->cfg.n_scenarios * s->L.bytes, s->stream),
                               "state reset");
   if (rc) return rc;
-  k_init<<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P);
+  if (s->L.N) k_init<true><<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P);
+  else k_init<false><<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P);
   return cuda_check(s, cudaGetLastError(), "k_init launch");
 }
 
@@ -507,7 +549,10 @@ dilu_status dilu_snapshot(dilu_sim* s, int32_t id_cap, int32_t* d_gpu, int32_t* 
   if (!s) return DILU_E_USAGE;
   if (s->status == DILU_E_CUDA) return DILU_E_STATE;
   if (id_cap < 0 || (id_cap > 0 && !d_inst && d_gpu == nullptr)) return fail(s, DILU_E_USAGE, "snapshot: bad args");
-  k_snapshot<<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P, id_cap, d_gpu, id_cap > 0 ? d_inst : nullptr);
+  if (s->L.N)
+    k_snapshot<true><<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P, id_cap, d_gpu, id_cap > 0 ? d_inst : nullptr);
+  else
+    k_snapshot<false><<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P, id_cap, d_gpu, id_cap > 0 ? d_inst : nullptr);
   dilu_status rc = cuda_check(s, cudaGetLastError(), "k_snapshot launch");
   if (rc) return rc;
   return cuda_check(s, cudaStreamSynchronize(s->stream), "snapshot sync");
@@ -571,6 +616,22 @@ dilu_status dilu_profile(const dilu_prof_session* d_sessions, int32_t n, dilu_pr
   long long blocks = (n + 255) / 256;
   if (blocks > (long long)n_sm * per) blocks = (long long)n_sm * per;
   prof::k_profile<<<(int)blocks, 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(d_sessions, n, d_out);
+  return cudaGetLastError() == cudaSuccess ? DILU_OK : DILU_E_CUDA;
+}
+
+dilu_status dilu_load_profiles(const dilu_catalog_row* d_cat, const dilu_prof_out* d_prof,
+                               int32_t n, int32_t slot_ms, dilu_func* d_out, int32_t* d_status,
+                               void* cuda_stream) {
+  if (n < 0 || slot_ms < 1 || slot_ms > 1000 || (n > 0 && (!d_cat || !d_prof || !d_out || !d_status)))
+    return DILU_E_USAGE;
+  if (n == 0) return DILU_OK;
+  int dev = 0, n_sm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  long long blocks = (n + 255) / 256;
+  if (blocks > (long long)n_sm * 8) blocks = (long long)n_sm * 8;
+  prof::k_load<<<(int)blocks, 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(d_cat, d_prof, n, slot_ms,
+                                                                                    d_out, d_status);
   return cudaGetLastError() == cudaSuccess ? DILU_OK : DILU_E_CUDA;
 }
 

@@ -125,3 +125,58 @@ __global__ void __launch_bounds__(256) k_profile(const dilu_prof_session* __rest
 
 }  // namespace prof
 }  // namespace dilu
+
+namespace dilu {
+namespace prof {
+
+static_assert(sizeof(dilu_catalog_row) == 72, "catalogue row layout");
+static_assert(sizeof(dilu_func) == 64, "function row layout");
+
+// Q25 ceiling of a non-negative fp64 quantity (ceil(x - 1e-9)), int32-saturated
+__device__ __forceinline__ int32_t q25_ceil(double x) {
+  const double y = ceil(__dsub_rn(x, 1e-9));
+  return y >= 2147483647.0 ? 2147483647 : (int32_t)y;
+}
+
+// a0: one thread per row (include/dilu.h dilu_load_profiles)
+__global__ void k_load(const dilu_catalog_row* __restrict__ cat, const dilu_prof_out* __restrict__ pr,
+                       int32_t n, int32_t slot_ms, dilu_func* __restrict__ out, int32_t* __restrict__ st) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const dilu_catalog_row c = cat[i];
+    const dilu_prof_out p = pr[i];
+    dilu_func r;
+    r.kind = -1; r.prio = c.prio; r.ibs = 0; r.req_pm = 0; r.lim_pm = 0; r.mem_mib = 0;
+    r.work_per_batch = 0; r.n_workers = 1; r.duty_pm = 0; r.cold_slots = 0;
+    r.affinity_class = c.affinity_class; r.arrive_sec = c.arrive_sec; r.depart_sec = c.depart_sec;
+    r.pattern = c.pattern; r.scale_q10 = c.scale_q10; r.phase_slots = c.phase_slots;
+    const bool train = c.kind == 2, inf = c.kind == 0 || c.kind == 1;
+    int32_t status = 0;
+    if (!(train || inf) || !(c.mem_gb >= 0.0) || !(c.cold_ms >= 0.0) || (inf && !(c.slo_ms >= 0.0)) ||
+        !isfinite(c.mem_gb) || !isfinite(c.cold_ms) || (inf && !isfinite(c.slo_ms)))
+      status = 2;
+    else if (p.status != 0)
+      status = 1;
+    else if (train != (p.ibs == 0))                 // training session <-> training row
+      status = 2;
+    if (status == 0) {
+      r.kind = c.kind;
+      r.req_pm = p.req_pm;                                        // Q25 (profiler)
+      r.lim_pm = p.lim_pm;
+      r.mem_mib = q25_ceil(__dmul_rn(1024.0, c.mem_gb));           // Q25
+      r.cold_slots = q25_ceil(__ddiv_rn(c.cold_ms, (double)slot_ms));
+      if (train) {
+        r.n_workers = c.n_workers;
+        r.duty_pm = c.duty_pm;
+      } else {
+        r.ibs = p.ibs;
+        const double cb = floor(__ddiv_rn(__dmul_rn((double)p.req_pm, c.slo_ms), 2.0));   // R4
+        r.work_per_batch = cb >= 2147483647.0 ? 2147483647 : (int32_t)cb;
+      }
+    }
+    out[i] = r;
+    st[i] = status;
+  }
+}
+
+}  // namespace prof
+}  // namespace dilu

@@ -27,6 +27,12 @@
 
 namespace dilu {
 
+#ifndef DILU_HOT_SMEM
+#define DILU_HOT_SMEM 0
+#endif
+// the shared-memory CTA kernels use the narrow state (ET<true>); everything else the wide
+typedef ViewT<DILU_HOT_SMEM != 0> View;
+
 struct Params {
   const int32_t* funcs;      // [S][F][16] input rows
   const int32_t* pat;        // [P][Tp]
@@ -170,8 +176,11 @@ struct Grp {
 // ------------------------------------------------------------------ scenario
 
 struct Scn {
-  View& v;                   // lives in shared memory (one per CTA), not in registers
-  const Params* P;
+  const Params* P;           // the kernel's __grid_constant__ parameter (constant bank)
+  uint8_t* gblock;           // this scenario's state block (cold region)
+  uint8_t* hot;              // its hot region: the shared-memory copy or gblock
+  int32_t* ring;             // this scenario's RPS rings [F][W]
+  const View* sv;            // DILU_VMODE 1/2: the view built once per scenario in shared memory
   Grp g;
   DPN(int32_t) members;      // gang member slots of the request being placed (group-visible, [64])
   int32_t* flag;             // group-visible broadcast word
@@ -179,6 +188,19 @@ struct Scn {
   const int32_t* frow;       // this scenario's input function rows [F][16]
   unsigned long long* lat;   // request-level latency accumulator (shared, [NLAT])
   int32_t scn_id, om, ga, mode;   // mode: baseline (0 Dilu, 1 Exclusive, 2 MPS-l, 3 MPS-r, 4 eager)
+  int32_t b1lo, b1hi;        // B1: this thread's contiguous function range (fixed per call)
+  // The view of the state, rebuilt where it is used: every array address is the Layout's
+  // offset (constant bank) from the dynamic shared memory (hot arrays, DILU_HOT_SMEM units)
+  // or from gblock -- no loads, nothing kept in shared memory or local memory.
+  __device__ __forceinline__ View view() const {
+    View v = make_view<DILU_HOT_SMEM != 0>(hot, gblock, P->L);
+#ifdef DILU_BOUNDS
+    v.ring = Chk<int32_t>(ring, (long long)P->F * P->W, v.ring.id);
+#else
+    v.ring = ring;
+#endif
+    return v;
+  }
 };
 enum : int32_t { M_DILU = 0, M_EXCLUSIVE = 1, M_STATIC_LIMIT = 2, M_STATIC_REQUEST = 3, M_EAGER = 4 };
 // literal Algorithm 2 at 5 ms periods (cfg.flags bit2; D8)
@@ -235,88 +257,43 @@ static __device__ int32_t g_scan(Scn& c, int32_t v, Red& red, int& ph, int32_t* 
 
 // ---- hot-region view ------------------------------------------------------------------
 // In translation units compiled with DILU_HOT_SMEM=1 (the k_run<true, *> kernels: the hot
-// region staged in shared memory) every hot-region pointer is asserted to be a shared-space
-// address, so the compiler emits LDS/STS/ATOMS instead of generic LD/ST/ATOM (29 vs 33
-// cycles per dependent load, tools/ubench/smem_chase.cu).  Functions take a register copy
-// of the view so the assertion reaches every access.  terminate_impl keeps generic
-// accesses: converted together with release (which it calls) it faulted at run time in C2
-// (either one alone is clean, as is every other combination tried) -- unresolved.
+// region staged in shared memory) every hot-region array of the view is an SPtr
+// (state.cuh) that asserts the shared window at each use, so the compiler emits
+// LDS/STS/ATOMS.  Functions work through a reference to the one shared View.
 #ifndef DILU_HOT_SMEM
 #define DILU_HOT_SMEM 0
 #endif
+#if DILU_VMODE == 1 && DILU_HOT_SMEM && !defined(DILU_BOUNDS)
+// mode 1: a register copy of the shared view whose hot pointers carry the shared-window
+// assertion (LDS/STS); the pointers are shared addresses by construction (run_scenario).
 static __device__ __forceinline__ View hot_view(const View& s) {
   View v = s;
-#if DILU_HOT_SMEM && !defined(DILU_BOUNDS)
 #define DILU_A(p) __builtin_assume(__isShared(v.p))
-  DILU_A(h);
-  DILU_A(gR);
-  DILU_A(gL);
-  DILU_A(gU);
-  DILU_A(gN);
-  DILU_A(gRes);
-  DILU_A(gExcl);
-  DILU_A(gGrow);
-  DILU_A(gMask);
-  DILU_A(rlG);
-  DILU_A(rlE);
-  DILU_A(iId);
-  DILU_A(iFunc);
-  DILU_A(iMeta);
-  DILU_A(iReady);
-  DILU_A(iNext);
-  DILU_A(iR);
-  DILU_A(fKind);
-  DILU_A(fReq);
-  DILU_A(fLim);
-  DILU_A(fMem);
-  DILU_A(fCb);
-  DILU_A(fIbs);
-  DILU_A(fNw);
-  DILU_A(fCls);
-  DILU_A(fDtr);
-  DILU_A(fPat);
-  DILU_A(fScale);
-  DILU_A(fPhase);
-  DILU_A(fCap1);
-  DILU_A(fReg);
-  DILU_A(fNsamp);
-  DILU_A(fAcc);
-  DILU_A(fHead);
-  DILU_A(fUp);
-  DILU_A(fDown);
-  DILU_A(fThrn);
-  DILU_A(fOld);
-  DILU_A(fPv);
-  DILU_A(fNlive);
-  DILU_A(fLh);
-  DILU_A(fGang);
-  DILU_A(fFlag);
-  DILU_A(fArr);
-  DILU_A(fDep);
-  DILU_A(fPidx);
-  DILU_A(fInfL);
-  DILU_A(fDefL);
-  DILU_A(gRel);
-  DILU_A(fLt);
-  DILU_A(fK);
-  DILU_A(fList);
-  DILU_A(fstack);
-  DILU_A(fPrio);
-  DILU_A(fCold);
-  DILU_A(qFunc);
-  DILU_A(qFirst);
-  DILU_A(qN);
-  DILU_A(qFail);
-  DILU_A(qSlot);
-  DILU_A(iQ);
+  DILU_A(h); DILU_A(gR); DILU_A(gL); DILU_A(gU); DILU_A(gRel); DILU_A(rlG); DILU_A(rlE);
+  DILU_A(gN); DILU_A(gNs); DILU_A(gExcl); DILU_A(gRes); DILU_A(gGrow); DILU_A(gMask);
+  DILU_A(iId); DILU_A(iReady); DILU_A(iR); DILU_A(iFunc); DILU_A(iNext); DILU_A(fstack); DILU_A(iMeta);
+  DILU_A(fKind); DILU_A(fPrio); DILU_A(fNw); DILU_A(fReq); DILU_A(fLim); DILU_A(fCb); DILU_A(fIbs);
+  DILU_A(fCls); DILU_A(fDtr); DILU_A(fPat); DILU_A(fScale); DILU_A(fCap1); DILU_A(fReg); DILU_A(fNsamp);
+  DILU_A(fHead); DILU_A(fUp); DILU_A(fDown); DILU_A(fFlag); DILU_A(fThrn); DILU_A(fNlive); DILU_A(fAcc);
+  DILU_A(fOld); DILU_A(fPv); DILU_A(fGang); DILU_A(fK); DILU_A(fArr); DILU_A(fDep); DILU_A(fPidx);
+  DILU_A(fLh); DILU_A(fLt); DILU_A(fList); DILU_A(fInfL); DILU_A(fDefL); DILU_A(qN); DILU_A(qFail);
+  DILU_A(qSlot); DILU_A(iQ);
 #undef DILU_A
-#endif
   return v;
 }
+#else
+static __device__ __forceinline__ const View& hot_view(const View& s) { return s; }
+#endif
+#if DILU_VMODE == 0        // rebuilt from the Layout in the kernel parameter
+#define DILU_VIEW(v, c) const View v = (c).view()
+#elif DILU_VMODE == 1      // register copy of the shared view, hot pointers asserted shared
+#define DILU_VIEW(v, c) const View v = hot_view(*(c).sv)
+#else                      // the shared view itself (SPtr offsets)
+#define DILU_VIEW(v, c) const View& v = *(c).sv
+#endif
+typedef DPN(int32_t) GP32;   // a generic (shared or global) int32 array
+#define DILU_CVIEW(v, c) DILU_VIEW(v, c)
 
-// DILU_VIEW(v, c): the view a function works through -- a register copy carrying the
-// shared-space assertion in DILU_HOT_SMEM units, else a plain reference (a copy only
-// costs registers when the state is in global memory).
 // Asynchronous 4-byte global -> shared copies (no register staging): the next second's
 // evicted ring sample (B1) and the next slot's pattern value (P0) land in the hot state
 // while the slot runs, so neither global load sits on a phase's critical path.  Each thread
@@ -328,23 +305,24 @@ static __device__ __forceinline__ void cp_async4(int32_t* sdst, const int32_t* g
 static __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
+static __device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N> static __device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory");
+}
 
-#if DILU_HOT_SMEM && !defined(DILU_BOUNDS)
-#define DILU_VIEW(v, c) View v = hot_view((c).v)
-#define DILU_CVIEW(v, c) const View v = hot_view((c).v)
-#else
-#define DILU_VIEW(v, c) View& v = (c).v
-#define DILU_CVIEW(v, c) const View& v = (c).v
-#endif
 
 // ---- serial helpers (thread 0 only) ------------------------------------------------
 
-static __device__ void list_append(View& v, int32_t f, int32_t s) {
+static __device__ void list_append(const View& v, int32_t f, int32_t s) {
   v.iNext[s] = -1;
+  __threadfence_block();   // pipelined slots: P0/P2 may walk the list meanwhile; the node
+                           // (pending, next = -1) is complete before it becomes reachable
   if (v.fLt[f] < 0) v.fLh[f] = s; else v.iNext[v.fLt[f]] = s;
   v.fLt[f] = s;
 }
-static __device__ void list_remove(View& v, int32_t f, int32_t s) {
+static __device__ void list_remove(const View& v, int32_t f, int32_t s) {
   int32_t prev = -1, cur = v.fLh[f];
   while (cur >= 0 && cur != s) { prev = cur; cur = v.iNext[cur]; }
   if (cur < 0) return;
@@ -367,7 +345,7 @@ static __device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
   v.gL[g] += v.fLim[f];
   v.gU[g] += share;
   v.h[H_SUMU] += share;
-  DPN(int32_t) res = v.gRes + (size_t)g * RES;
+  const auto res = v.gRes + (size_t)g * RES;
   int pos = v.gN[g];
   if (!c.P->ovl) {            // keep (prio, id) order now ...
     const long long k = res_key(v, s);
@@ -401,7 +379,7 @@ static __device__ void release(Scn& c, int32_t s) {
     v.gL[g] -= v.fLim[f];
     v.gU[g] -= sh;
     v.h[H_SUMU] -= sh;
-    DPN(int32_t) res = v.gRes + (size_t)g * RES;
+    const auto res = v.gRes + (size_t)g * RES;
     int j = 0;
     const int nr = v.gN[g];
     while (j < nr && res[j] != s) ++j;
@@ -432,11 +410,7 @@ static __device__ void terminate(Scn& c, int32_t s) {
   TSTOP(15);
 }
 static __device__ void terminate_impl(Scn& c, int32_t s) {
-#ifdef DILU_TERM_SMEM
   DILU_VIEW(v, c);
-#else
-  View& v = c.v;
-#endif
   const int32_t f = v.iFunc[s];
   if (st_of(v.iMeta[s]) == ST_PLACED) {
     const int32_t ep = ++v.h[H_EPOCH];   // room was freed: queued failures may now succeed
@@ -447,7 +421,7 @@ static __device__ void terminate_impl(Scn& c, int32_t s) {
       if (g < 0 || g >= c.P->G)
         printf("TERM_PROBE scn %d s %d k %d ns %d g %d meta %d id %d func %d gRel %p iG %p iMeta %p sv.iG %p\n",
                c.scn_id, s, k, ns, g, v.iMeta[s], v.iId[s], v.iFunc[s], (void*)v.gRel, (void*)v.iG,
-               (void*)v.iMeta, (void*)c.v.iG);
+               (void*)v.iMeta, (void*)v.iG);
 #endif
       v.gRel[g] = ep;
       const int32_t slot = v.h[H_RLN]++ % RLOG;
@@ -463,13 +437,13 @@ static __device__ void terminate_impl(Scn& c, int32_t s) {
   v.fstack[v.h[H_FSTOP]++] = s;
 }
 
-static __device__ void compact_queue(View& v) {
+static __device__ void compact_queue(const View& v) {
   const int32_t n = v.h[H_QLEN];
   int32_t k = 0;
   for (int32_t q = 0; q < n; ++q) {
     if (v.qN[q] == 0) continue;
     if (k != q) {
-      v.qFunc[k] = v.qFunc[q]; v.qFirst[k] = v.qFirst[q]; v.qN[k] = v.qN[q]; v.qFail[k] = v.qFail[q];
+      v.qN[k] = v.qN[q]; v.qFail[k] = v.qFail[q];
       v.qSlot[k] = v.qSlot[q];
       v.iQ[v.qSlot[k]] = k;
     }
@@ -513,11 +487,11 @@ static __device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
     v.fNlive[f] += 1;
     v.h[H_NLIVE] += 1;
   }
-  v.qFunc[q] = f; v.qFirst[q] = first; v.qN[q] = n; v.qFail[q] = -1;
+  v.qN[q] = n; v.qFail[q] = -1;
   return first;
 }
 
-static __device__ void register_func(View& v, int32_t f, int32_t t, int32_t Tp) {
+static __device__ void register_func(const View& v, int32_t f, int32_t t, int32_t Tp) {
   if (v.fReg[f]) return;
   v.fReg[f] = 1;
   v.fNsamp[f] = 0; v.fAcc[f] = 0; v.fHead[f] = 0; v.fUp[f] = 0; v.fDown[f] = 0;
@@ -526,20 +500,10 @@ static __device__ void register_func(View& v, int32_t f, int32_t t, int32_t Tp) 
   v.fPidx[f] = (int32_t)(((long long)t + v.fPhase[f]) % Tp);   // arrivals index for slot t
 }
 
-static __device__ void kill_queue_entries_of(View& v, int32_t f) {
+static __device__ void kill_queue_entries_of(const View& v, int32_t f) {
   const int32_t n = v.h[H_QLEN];
   for (int32_t q = 0; q < n; ++q)
-    if (v.qN[q] > 0 && v.qFunc[q] == f) { v.qN[q] = 0; v.h[H_QLIVE] -= 1; }
-}
-
-static __device__ void kill_queue_entry_with_id(View& v, int32_t id) {
-  const int32_t n = v.h[H_QLEN];
-  for (int32_t q = 0; q < n; ++q)
-    if (v.qN[q] > 0 && v.qFirst[q] <= id && id < v.qFirst[q] + v.qN[q]) {
-      v.qN[q] = 0;
-      v.h[H_QLIVE] -= 1;
-      return;
-    }
+    if (v.qN[q] > 0 && v.iFunc[v.qSlot[q]] == f) { v.qN[q] = 0; v.h[H_QLIVE] -= 1; }
 }
 
 // ---- placement (collective) --------------------------------------------------------
@@ -594,7 +558,7 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
     } else {
       const int32_t R = v.gR[g] + req, Lm = v.gL[g] + lim, U = v.gU[g] + mem;
       if (!(R <= c.om && Lm <= c.ga && U <= P.M && n < RES)) continue;
-      const DPN(int32_t) res = v.gRes + (size_t)g * RES;
+      const auto res = v.gRes + (size_t)g * RES;
       // affinity: the class bitmask rules most GPUs out exactly; scan on a hit
       int aff = 0;
       if ((v.gMask[g] >> (cls & 63)) & 1ull)
@@ -714,7 +678,7 @@ static __device__ int32_t next_attempt(Scn& c, int32_t q, int32_t qn, Acc& acc) 
       else if (fe == ep) cls = 1;                // nothing released since its failure
       else {
         ++nhope;
-        cls = hope_after(c, fe, v.qFunc[qq]) ? 2 : 1;
+        cls = hope_after(c, fe, v.iFunc[v.qSlot[qq]]) ? 2 : 1;
         stamp = cls == 1;
       }
     }
@@ -760,7 +724,7 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
       if (WARP && prev >= 0)                  // clear I* marks: every lane clears a stride
         for (int32_t g = threadIdx.x; g < c.P->G; g += 32) v.gExcl[g] = 0;   // (no iG loads)
       if (PG::leader(c) && prev >= 0) {
-        const int32_t n = v.qN[prev], f = v.qFunc[prev];
+        const int32_t n = v.qN[prev], f = v.iFunc[v.qSlot[prev]];
         if (!WARP)
           for (int j = 0; j < prev_placed; ++j) {   // clear I* marks
             const int32_t s = c.members[j];
@@ -804,7 +768,7 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
         c.flag[0] = e;
         c.flag[1] = qn;
         if (e < qn) {                   // gang members, ascending id
-          const int32_t n = v.qN[e], f = v.qFunc[e], first = v.qFirst[e];
+          const int32_t n = v.qN[e], s0 = v.qSlot[e], f = v.iFunc[s0], first = v.iId[s0];
           int j = 0;
           for (int32_t s = v.fLh[f]; s >= 0 && j < n; s = v.iNext[s]) {
             const int32_t id = v.iId[s];
@@ -865,7 +829,7 @@ static __device__ void rebuild_layout(Scn& c) {
   for (int32_t g = c.g.rank(); g < P.G; g += c.g.size()) {
     const int32_t n = v.gN[g];
     if (P.ovl && n > 1) {     // overlapped slots append commits: restore (prio, id) order
-      DPN(int32_t) res = v.gRes + (size_t)g * RES;
+      const auto res = v.gRes + (size_t)g * RES;
       long long kp = res_key(v, res[0]);
       for (int j = 1; j < n; ++j) {
         const int32_t s = res[j];
@@ -975,17 +939,17 @@ template <bool LAT>
 static __device__ void phase0(Scn& c, int32_t t, Acc& acc) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
-  DP(const int32_t) infl = v.fInfL;
-  DP(const int32_t) reg = v.fReg;
-  DP(const int32_t) fpat = v.fPat;
-  DP(const int32_t) fscale = v.fScale;
-  DP(int32_t) pidx = v.fPidx;
-  DP(int32_t) facc = v.fAcc;
-  DP(const int32_t) lh = v.fLh;
-  DP(const int32_t) nxt = v.iNext;
-  DP(const int32_t) meta = v.iMeta;
-  DP(const int32_t) ready = v.iReady;
-  DP(int32_t) r = v.iR + (P.SPS == 1 ? 0 : (t & 1)) * P.I;   // see phase1
+  const auto infl = v.fInfL;
+  const auto reg = v.fReg;
+  const auto fpat = v.fPat;
+  const auto fscale = v.fScale;
+  const auto pidx = v.fPidx;
+  const auto facc = v.fAcc;
+  const auto lh = v.fLh;
+  const auto nxt = v.iNext;
+  const auto meta = v.iMeta;
+  const auto ready = v.iReady;
+  const auto r = v.iR + (P.SPS == 1 ? 0 : (t & 1)) * P.I;   // see phase1
   const int32_t* __restrict__ gpat = P.pat;
   const int32_t Tp = P.Tp, ninf = v.h[H_NINF];
 #if DILU_HOT_SMEM
@@ -1026,6 +990,9 @@ static __device__ void phase0(Scn& c, int32_t t, Acc& acc) {
       }
     }
   }
+#if DILU_HOT_SMEM
+  cp_async_commit();                       // this slot's fPv copies: one group
+#endif
 }
 
 // P1: vertical token allocation per GPU row (Q13, Q14)
@@ -1040,27 +1007,27 @@ static __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
   // the LLM stage minima use the other half of iR (shared memory) instead of the cold
   // double buffer iBmin.
   const bool one = P.SPS == 1;
-  DP(const int32_t) r = v.iR + (one ? 0 : par) * P.I;
-  DPN(int32_t) bmin = one ? v.iR + P.I : v.iBmin + par * P.I;
-  DPN(int32_t) gang = v.fGang + par * P.F;
-  DP(const int32_t) grow = v.gGrow;
+  const auto r = v.iR + (one ? 0 : par) * P.I;
+  DPN(int32_t) bmin = one ? GP32(v.iR + P.I) : GP32(v.iBmin + par * P.I);
+  const auto gang = v.fGang + par * P.F;
+  const auto grow = v.gGrow;
   // row sizes as of the last repack: in overlapped slots warp 0 appends (cold) residents
   // beyond them while this runs; rows below gNs never move (commit)
-  DP(const int32_t) gn = v.gNs;
-  DP(const int32_t) gres = v.gRes;
-  DP(const int32_t) meta_ = v.iMeta;
-  DP(const int32_t) ready = v.iReady;
-  DP(const int32_t) ifunc = v.iFunc;
-  DP(const int32_t) iid = v.iId;
-  DP(const int32_t) fkind = v.fKind;
-  DP(const int32_t) freq = v.fReq;
-  DP(const int32_t) flim = v.fLim;
-  DP(const int32_t) fdtr = v.fDtr;
-  DP(const int32_t) fibs = v.fIbs;
-  DP(const int32_t) fcb = v.fCb;
-  DP(const int32_t) cbase = v.h + H_CBASE;
-  DP(const int32_t) ccnt = v.h + H_CCNT;
-  DP(const int32_t) gbase = v.h + H_GBASE;
+  const auto gn = v.gNs;
+  const auto gres = v.gRes;
+  const auto meta_ = v.iMeta;
+  const auto ready = v.iReady;
+  const auto ifunc = v.iFunc;
+  const auto iid = v.iId;
+  const auto fkind = v.fKind;
+  const auto freq = v.fReq;
+  const auto flim = v.fLim;
+  const auto fdtr = v.fDtr;
+  const auto fibs = v.fIbs;
+  const auto fcb = v.fCb;
+  const auto cbase = v.h + H_CBASE;
+  const auto ccnt = v.h + H_CCNT;
+  const auto gbase = v.h + H_GBASE;
   const int32_t nch = cbase[6];
   const int32_t T = (int32_t)P.T_slot, slot_ms = P.slot_ms;
   const uint64_t ht = sm64(sm64((uint32_t)c.scn_id) ^ (uint32_t)t);   // mix() prefix, per slot
@@ -1148,14 +1115,14 @@ static __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
   const Params& P = *c.P;
   const int par = t & 1;
   const bool one = P.SPS == 1;          // buffers as in phase1
-  DP(const int32_t) r = v.iR + (one ? 0 : par) * P.I;
-  DPN(int32_t) bmin = one ? v.iR + P.I : v.iBmin + par * P.I;
-  DPN(int32_t) gang = v.fGang + par * P.F;
-  DP(const int32_t) defl = v.fDefL;
-  DP(const int32_t) reg = v.fReg;
-  DP(const int32_t) lh = v.fLh;
-  DP(const int32_t) nxt = v.iNext;
-  DP(const int32_t) meta = v.iMeta;
+  const auto r = v.iR + (one ? 0 : par) * P.I;
+  DPN(int32_t) bmin = one ? GP32(v.iR + P.I) : GP32(v.iBmin + par * P.I);
+  const auto gang = v.fGang + par * P.F;
+  const auto defl = v.fDefL;
+  const auto reg = v.fReg;
+  const auto lh = v.fLh;
+  const auto nxt = v.iNext;
+  const auto meta = v.iMeta;
   const int32_t ndef = v.h[H_NDEF];
   for (int32_t k = c.g.rank(); k < ndef; k += c.g.size()) {
     const int32_t f = defl[k];
@@ -1218,14 +1185,14 @@ template <bool LAT>
 static __device__ void phase0_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
-  DP(const int32_t) infl = v.fInfL;
-  DP(const int32_t) reg = v.fReg;
-  DP(int32_t) pidx = v.fPidx;
-  DP(const int32_t) lh = v.fLh;
-  DP(const int32_t) nxt = v.iNext;
-  DP(const int32_t) meta = v.iMeta;
-  DP(const int32_t) ready = v.iReady;
-  DP(int32_t) rb = v.rB;
+  const auto infl = v.fInfL;
+  const auto reg = v.fReg;
+  const auto pidx = v.fPidx;
+  const auto lh = v.fLh;
+  const auto nxt = v.iNext;
+  const auto meta = v.iMeta;
+  const auto ready = v.iReady;
+  const auto rb = v.rB;
   const int32_t Tp = P.Tp, ninf = v.h[H_NINF], I = P.I;
   for (int32_t k = c.g.rank(); k < ninf; k += c.g.size()) {
     const int32_t f = infl[k];
@@ -1263,7 +1230,7 @@ static __device__ void phase0_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
       }
       const int32_t q = A / nw, rem = A - q * nw;
       int32_t rank = 0;
-      DP(int32_t) ru = rb + (size_t)u * I;
+      const auto ru = rb + (size_t)u * I;
       for (int32_t s = s0; s >= 0; s = nxt[s]) {
         if (st_of(meta[s]) == ST_PLACED && ready[s] <= tu) {
           ru[s] = q + (rank < rem ? 1 : 0);
@@ -1281,9 +1248,9 @@ static __device__ void phase1_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
-  DP(const int32_t) cbase = v.h + H_CBASE;
-  DP(const int32_t) ccnt = v.h + H_CCNT;
-  DP(const int32_t) gbase = v.h + H_GBASE;
+  const auto cbase = v.h + H_CBASE;
+  const auto ccnt = v.h + H_CCNT;
+  const auto gbase = v.h + H_GBASE;
   const int32_t nch = cbase[6];
   const int32_t T = (int32_t)P.T_slot, slot_ms = P.slot_ms, I = P.I, F = P.F;
   const uint64_t hs = sm64((uint32_t)c.scn_id);
@@ -1383,10 +1350,10 @@ template <bool LAT>
 static __device__ void phase2_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
-  DP(const int32_t) defl = v.fDefL;
-  DP(const int32_t) lh = v.fLh;
-  DP(const int32_t) nxt = v.iNext;
-  DP(const int32_t) meta = v.iMeta;
+  const auto defl = v.fDefL;
+  const auto lh = v.fLh;
+  const auto nxt = v.iNext;
+  const auto meta = v.iMeta;
   const int32_t ndef = v.h[H_NDEF], I = P.I, F = P.F;
   for (int32_t k = c.g.rank(); k < ndef; k += c.g.size()) {
     const int32_t f = defl[k];
@@ -1462,9 +1429,9 @@ static __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, DPN(const int32
   const Params& P = *c.P;
   const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
   const unsigned FULL = 0xffffffffu;
-  DP(const int32_t) cbase = v.h + H_CBASE;
-  DP(const int32_t) ccnt = v.h + H_CCNT;
-  DP(const int32_t) gbase = v.h + H_GBASE;
+  const auto cbase = v.h + H_CBASE;
+  const auto ccnt = v.h + H_CCNT;
+  const auto gbase = v.h + H_GBASE;
   const int32_t nch = cbase[6];
   const int32_t NP = P.slot_ms / A2_PERIOD_MS;
   const long long PT = (long long)A2_PERIOD_MS * 1000;          // period in us
@@ -1661,108 +1628,210 @@ static __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, DPN(const int32
 
 enum : int32_t { EV_DEP = 1, EV_OUT = 2, EV_IN = 4, EV_ARR = 8 };
 
+// B1 for one function f at the boundary of second `sec`: window push of second sec-1,
+// incremental up/down counts, the lazy (or eager) scaling decision, departure / arrival
+// flags.  Writes fFlag[f]; returns the flags.  The
+// fOld prefetch is issued and consumed by the same thread (fixed f -> thread mapping).
+static __device__ int32_t b1_func(Scn& c, int32_t f, int32_t sec) {
+  DILU_VIEW(v, c);
+  const Params& P = *c.P;
+  const int32_t W = P.W;
+  const int32_t kind = v.fKind[f];
+  int32_t ev = 0;
+  if (kind != K_UNUSED) {
+    if (v.fReg[f]) {
+      const bool inf = is_inf(kind);
+      const auto ring = v.ring + (size_t)f * W;
+      const long long cap1 = v.fCap1[f];
+      int32_t last = 0;
+      if (inf && sec >= 1) {                      // step 1: push second sec-1
+        const int32_t val = v.fAcc[f];
+        last = val;
+        const int32_t head = v.fHead[f];
+        const int32_t ns = v.fNsamp[f];
+        const int32_t thr = v.fThrn[f];
+        if (thr >= 0) {
+          const long long cu = (long long)thr * cap1, cd = (long long)(thr - 1) * cap1;
+          int32_t du = val > cu, dd = val < cd;
+          if (ns >= W) {
+#if DILU_HOT_SMEM
+            const int32_t old = W > 1 ? v.fOld[f] : ring[head];   // prefetched last second
+#else
+            const int32_t old = ring[head];
+#endif
+            du -= old > cu; dd -= old < cd;
+          }
+          v.fUp[f] += du;
+          v.fDown[f] += dd;
+        }
+        ring[head] = val;
+        const int32_t nhead = head + 1 == W ? 0 : head + 1;
+        v.fHead[f] = nhead;
+#if DILU_HOT_SMEM
+        if (W > 1) cp_async4(v.fOld + f, ring + nhead);        // next second's evictee
+#endif
+        v.fNsamp[f] = ns < W ? ns + 1 : W;     // saturating: only >= W / >= 1 matter
+        v.fAcc[f] = 0;
+      }
+      if (v.fDep[f] == sec) {                     // step 2: departure
+        ev = EV_DEP;
+      } else if (inf && c.mode == M_EAGER) {      // reactive scaling on the last sample
+        if (v.fNsamp[f] >= 1) {
+          const int32_t n = v.fNlive[f];
+          if ((long long)last > (long long)n * cap1) {
+            const long long k = ((long long)last + cap1 - 1) / cap1 - n;
+            if (k >= 1) { ev = EV_OUT; v.fK[f] = (int32_t)k; }
+          } else if ((long long)last < (long long)(n - 1) * cap1 && n > P.min_inst) {
+            ev = EV_IN;
+          }
+        }
+      } else if (inf && v.fNsamp[f] >= W) {       // step 3: lazy scaling decision
+        const int32_t n = v.fNlive[f];
+        const long long cu = (long long)n * cap1, cd = (long long)(n - 1) * cap1;
+        if (v.fThrn[f] != n) {
+          int32_t up = 0, dn = 0;
+          for (int j = 0; j < W; ++j) { const int32_t w = ring[j]; up += w > cu; dn += w < cd; }
+          v.fUp[f] = up; v.fDown[f] = dn; v.fThrn[f] = n;
+        }
+        if (v.fUp[f] >= P.phi_out) {
+          int32_t mx = 0;
+          for (int j = 0; j < W; ++j) mx = max(mx, ring[j]);
+          const long long k = ((long long)mx + cap1 - 1) / cap1 - n;
+          if (k >= 1) { ev = EV_OUT; v.fK[f] = (int32_t)k; }
+        } else if (v.fDown[f] > P.phi_in && n > P.min_inst) {
+          ev = EV_IN;
+        }
+      }
+    }
+    if (v.fArr[f] == sec) ev |= EV_ARR;           // step 4: arrival
+  }
+  v.fFlag[f] = ev;
+  return ev;
+}
+
+// B1 share of one boundary (pipelined slots): every thread pushes and
+// decides its own contiguous function range [b1lo, b1hi) (the same range every call, so
+// the thread that issues a function's fOld prefetch is the one that consumes it).  Workers
+// run it right after P0 (ALLOW = 1: P0's fPv copies, the last committed group, may stay in
+// flight), warp 0 after its placement pass (ALLOW = 0).  Flags land in fFlag.
+template <int ALLOW>
+static __device__ void b1_share(Scn& c, int32_t t) {
+  const Params& P = *c.P;
+  const int32_t sec = P.SPS == 1 ? t : t / P.SPS;
+#if DILU_HOT_SMEM
+  cp_async_wait_group<ALLOW>();                    // this thread's last fOld copies landed
+#endif
+  for (int32_t f = c.b1lo; f < c.b1hi; ++f) b1_func(c, f, sec);
+#if DILU_HOT_SMEM
+  cp_async_commit();
+#endif
+}
+
+// Ordered event list of the boundary from fFlag (warp 0: one ballot per 32 functions);
+// returns the event count (uniform over the warp).
+static __device__ int32_t compact_events(Scn& c) {
+  DILU_VIEW(v, c);
+  const Params& P = *c.P;
+  const int lane = threadIdx.x & 31;
+  int32_t cnt = 0;
+  for (int32_t base = 0; base < P.F; base += 32) {
+    const int32_t f = base + lane;
+    const bool ev = f < P.F && v.fFlag[f] != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, ev);
+    if (ev) v.fList[cnt + __popc(m & ((1u << lane) - 1))] = f;
+    cnt += __popc(m);
+  }
+  return cnt;
+}
+
+// ---- pipelined slots: B3 split around the control arm --------------------
+// B3a (leader, before the slot's barrier): the state-removing half of the boundary's events
+// in the paper's order -- departures (queue entries dropped, instances released), scale-in
+// victims -- plus the registration of arriving functions (P0 of this slot sees them) and the
+// capacity rule evaluated in the paper's order (live instances may not exceed max_instances
+// at any enqueue; D3).  The enqueues themselves (scale-outs, then arrivals, each
+// in function order: the ids the paper's order assigns) run in b3b inside the control arm,
+// where only pending (not warm) instances appear beside the running P0/P1/P2.
+static __device__ void b3a(Scn& c, int32_t t, int32_t total, Acc& acc) {
+  DILU_VIEW(v, c);
+  const Params& P = *c.P;
+  acc.z->st[S_EVENT] += total;
+  long long live = v.h[H_NLIVE];
+  for (int32_t e = 0; e < total; ++e) {          // step 2: departures
+    const int32_t f = v.fList[e];
+    if (!(v.fFlag[f] & EV_DEP)) continue;
+    live -= v.fNlive[f];
+    kill_queue_entries_of(v, f);
+    while (v.fLh[f] >= 0) terminate(c, v.fLh[f]);
+    v.fReg[f] = 0;
+  }
+  bool err = false;
+  for (int32_t e = 0; e < total && !err; ++e) {  // step 3: hscaler actions
+    const int32_t f = v.fList[e];
+    const int32_t ev = v.fFlag[f];
+    if (ev & EV_OUT) {
+      const int32_t k = v.fK[f];
+      for (int32_t j = 0; j < k && !err; ++j) { if (live + 1 > P.I) err = true; else live += 1; }
+      acc.z->sout += 1;
+    } else if (ev & EV_IN) {
+      const int32_t victim = v.fLt[f];           // highest live id (Q19)
+      if (st_of(v.iMeta[victim]) == ST_PEND) {   // its own request
+        v.qN[v.iQ[victim]] = 0;
+        v.h[H_QLIVE] -= 1;
+      }
+      terminate(c, victim);
+      live -= 1;
+      acc.z->sin += 1;
+    }
+  }
+  for (int32_t e = 0; e < total && !err; ++e) {  // step 4: arrivals (registration)
+    const int32_t f = v.fList[e];
+    if (!(v.fFlag[f] & EV_ARR)) continue;
+    register_func(v, f, t, P.Tp);
+    if (v.fKind[f] == K_TRAIN) {
+      if (live + v.fNw[f] > P.I) err = true; else live += v.fNw[f];
+    } else {
+      for (int32_t j = 0; j < P.min_inst && !err; ++j) { if (live + 1 > P.I) err = true; else live += 1; }
+    }
+  }
+  if (err) v.h[H_ERR] = 6;
+}
+
+// B3b (leader, control arm): the deferred enqueues of b3a's boundary, in the paper's order.
+static __device__ void b3b(Scn& c, int32_t total) {
+  DILU_VIEW(v, c);
+  const Params& P = *c.P;
+  for (int32_t e = 0; e < total; ++e) {
+    const int32_t f = v.fList[e];
+    if (v.fFlag[f] & EV_OUT)
+      for (int32_t j = 0; j < v.fK[f]; ++j) enqueue(c, f, 1);
+  }
+  for (int32_t e = 0; e < total; ++e) {
+    const int32_t f = v.fList[e];
+    if (!(v.fFlag[f] & EV_ARR)) continue;
+    if (v.fKind[f] == K_TRAIN) enqueue(c, f, v.fNw[f]);
+    else for (int32_t j = 0; j < P.min_inst; ++j) enqueue(c, f, 1);
+  }
+}
+
 // Returns whether a placement pass is due.  ovl (overlapped slots): the pass is left to
 // the caller, which runs it in warp 0 beside P0/P1/P2.
 static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, bool ovl = false) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
-  const int32_t sec = t / P.SPS;
+  const int32_t sec = P.SPS == 1 ? t : t / P.SPS;
   // B1 (function-parallel): window push, incremental counts, decisions, event flags.
   // Contiguous function ranges per thread keep the event list in ascending order.
-  DP(const int32_t) fkind = v.fKind;
-  DP(int32_t) reg = v.fReg;
-  DP(const int32_t) farr = v.fArr;
-  DP(const int32_t) fdep = v.fDep;
-  DP(const int64_t) fcap1 = v.fCap1;
-  DP(int32_t) facc = v.fAcc;
-  DP(int32_t) fhead = v.fHead;
-  DP(int32_t) fns = v.fNsamp;
-  DP(int32_t) fthr = v.fThrn;
-  DP(int32_t) fup = v.fUp;
-  DP(int32_t) fdown = v.fDown;
-  DP(const int32_t) fnlive = v.fNlive;
-  DP(int32_t) fflag = v.fFlag;
-  DP(int32_t) ringb = v.ring;
-  const int32_t W = P.W;
-  const int32_t per = (P.F + c.g.size() - 1) / c.g.size();
-  const int32_t lo = c.g.rank() * per, hi = min(P.F, lo + per);
+  const int32_t lo = c.b1lo, hi = c.b1hi;   // this thread's contiguous function range
+  const auto fflag = v.fFlag;
   int32_t cnt = 0;
 #if DILU_HOT_SMEM
   cp_async_wait_all();                              // this thread's fOld / fPv copies landed
 #endif
-  for (int32_t f = lo; f < hi; ++f) {
-    const int32_t kind = fkind[f];
-    int32_t ev = 0;
-    if (kind != K_UNUSED) {
-      if (reg[f]) {
-        const bool inf = is_inf(kind);
-        DPN(int32_t) ring = ringb + (size_t)f * W;
-        const long long cap1 = fcap1[f];
-        int32_t last = 0;
-        if (inf && sec >= 1) {                      // step 1: push second sec-1
-          const int32_t val = facc[f];
-          last = val;
-          const int32_t head = fhead[f];
-          const int32_t ns = fns[f];
-          const int32_t thr = fthr[f];
-          if (thr >= 0) {
-            const long long cu = (long long)thr * cap1, cd = (long long)(thr - 1) * cap1;
-            int32_t du = val > cu, dd = val < cd;
-            if (ns >= W) {
+  for (int32_t f = lo; f < hi; ++f) cnt += b1_func(c, f, sec) != 0;
 #if DILU_HOT_SMEM
-              const int32_t old = W > 1 ? v.fOld[f] : ring[head];   // prefetched last second
-#else
-              const int32_t old = ring[head];
+  cp_async_commit();
 #endif
-              du -= old > cu; dd -= old < cd;
-            }
-            fup[f] += du;
-            fdown[f] += dd;
-          }
-          ring[head] = val;
-          const int32_t nhead = head + 1 == W ? 0 : head + 1;
-          fhead[f] = nhead;
-#if DILU_HOT_SMEM
-          if (W > 1) cp_async4(v.fOld + f, ring + nhead);        // next second's evictee
-#endif
-          fns[f] = ns + 1;
-          facc[f] = 0;
-        }
-        if (fdep[f] == sec) {                       // step 2: departure
-          ev = EV_DEP;
-        } else if (inf && c.mode == M_EAGER) {      // reactive scaling on the last sample
-          if (fns[f] >= 1) {
-            const int32_t n = fnlive[f];
-            if ((long long)last > (long long)n * cap1) {
-              const long long k = ((long long)last + cap1 - 1) / cap1 - n;
-              if (k >= 1) { ev = EV_OUT; v.fK[f] = (int32_t)k; }
-            } else if ((long long)last < (long long)(n - 1) * cap1 && n > P.min_inst) {
-              ev = EV_IN;
-            }
-          }
-        } else if (inf && fns[f] >= W) {            // step 3: lazy scaling decision
-          const int32_t n = fnlive[f];
-          const long long cu = (long long)n * cap1, cd = (long long)(n - 1) * cap1;
-          if (fthr[f] != n) {
-            int32_t up = 0, dn = 0;
-            for (int j = 0; j < W; ++j) { const int32_t w = ring[j]; up += w > cu; dn += w < cd; }
-            fup[f] = up; fdown[f] = dn; fthr[f] = n;
-          }
-          if (fup[f] >= P.phi_out) {
-            int32_t mx = 0;
-            for (int j = 0; j < W; ++j) mx = max(mx, ring[j]);
-            const long long k = ((long long)mx + cap1 - 1) / cap1 - n;
-            if (k >= 1) { ev = EV_OUT; v.fK[f] = (int32_t)k; }
-          } else if (fdown[f] > P.phi_in && n > P.min_inst) {
-            ev = EV_IN;
-          }
-        }
-      }
-      if (farr[f] == sec) ev |= EV_ARR;             // step 4: arrival
-    }
-    fflag[f] = ev;
-    cnt += ev != 0;
-  }
 #ifdef DILU_PHASE_TIMING
   const long long cb0 = clock64();   // st[22]: B1 count barrier -> end of compaction (leader)
 #endif
@@ -1842,7 +1911,7 @@ static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
 // (cfg.flags bit2).  Separate instantiations, so the one-slot-per-second slot-model kernels
 // (C1-C4) carry neither the batch nor the period code.
 template <bool SMEM, int VAR>
-static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t* smem, int32_t sc, int32_t t0,
+static __device__ void run_scenario(const Params& P, Red& red, View* sv, uint8_t* smem, int32_t sc, int32_t t0,
                              int32_t n_slots, int32_t n_req, const int32_t* req_scn,
                              const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid,
                              int K = 1, int crank = 0) {
@@ -1854,15 +1923,21 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
     for (size_t k = threadIdx.x; k < P.L.hot_bytes / 16; k += blockDim.x) dst[k] = src[k];
     hot = smem;
   }
+  Scn c;
+  c.gblock = gblock;
+  c.hot = hot;
+  c.sv = sv;
+#if DILU_VMODE != 0
   if (threadIdx.x == 0) {
-    sv = make_view(hot, gblock, P.L);
+    *sv = make_view<DILU_HOT_SMEM != 0>(hot, gblock, P.L);
 #ifdef DILU_BOUNDS
-    sv.ring = Chk<int32_t>(P.ring + (size_t)sc * P.F * P.W, (long long)P.F * P.W, sv.ring.id);
+    sv->ring = Chk<int32_t>(P.ring + (size_t)sc * P.F * P.W, (long long)P.F * P.W, sv->ring.id);
 #else
-    sv.ring = P.ring + (size_t)sc * P.F * P.W;
+    sv->ring = P.ring + (size_t)sc * P.F * P.W;
 #endif
   }
-  Scn c{sv};
+#endif
+  c.ring = P.ring + (size_t)sc * P.F * P.W;
   c.P = &P;
   c.g.K = K;
   c.g.crank = crank;
@@ -1878,6 +1953,11 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
 #endif
   c.flag = K == 1 ? red.flag : reinterpret_cast<int32_t*>(c.g.gu + 80);
   c.frow = P.funcs + (size_t)sc * P.F * 16;
+  {
+    const int32_t per = (P.F + c.g.size() - 1) / c.g.size();
+    c.b1lo = min(P.F, c.g.rank() * per);
+    c.b1hi = min(P.F, c.b1lo + per);
+  }
   c.scn_id = P.scen[sc * 4 + 0];
   c.om = P.scen[sc * 4 + 1];
   c.ga = P.scen[sc * 4 + 2];
@@ -1891,7 +1971,7 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
     for (int k = threadIdx.x; k < NLAT; k += blockDim.x) red.lat[k] = 0;
   int ph = 0;
   __syncthreads();
-  DILU_VIEW(v, c);            // after the barrier: thread 0 built the shared view
+  DILU_VIEW(v, c);
   if (v.h[H_ERR]) return;     // uniform: nobody has written since the group started
 
   if (n_req >= 0) {
@@ -1934,10 +2014,102 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
       // host's P.ovl): what the pass commits is cold in this slot, so P0/P1/P2 never count
       // it; pending instances read as not ready (iReady = BIG), rows only grow past gNs.
       const bool ovl = !fused && !alg2 && !lat && P.ovl;
+      if (ovl && P.ovl == 2) {
+        // Pipelined slot.  Serial part: warp 0 compacts the boundary's event
+        // flags (written by the previous slot's B1 shares), the leader applies B3a, one
+        // barrier, repack if residency changed.  Then two arms: warp 0 = control (B3b
+        // enqueues, the placement pass, the active-set fold, its B1 share of the next
+        // boundary once P0 has folded this slot's arrivals into fAcc), warps 1.. = P0 ->
+        // their B1 shares -> P1 -> P2 on the state after B3a.  One join barrier.
+        const bool bnd = P.SPS == 1 || t % P.SPS == 0;
+        TICK(0);
+        if (bnd && t == t0) {                            // prologue: this call's first B1
+          b1_share<0>(c, t);
+          __syncthreads();
+        }
+        int32_t total = 0;
+        if (bnd) {
+          if (threadIdx.x < 32) {
+            total = compact_events(c);
+            if (total > 0 && c.g.leader()) b3a(c, t, total, acc);
+            if (threadIdx.x == 0) v.h[H_PNEV] = total;
+          }
+          __syncthreads();
+          total = v.h[H_PNEV];
+          if (v.h[H_ERR]) break;                         // uniform after the barrier
+        }
+        const bool pass = bnd && (total > 0 || v.h[H_QLEN] > 0);
+        TICK(1);
+        if (v.h[H_DIRTY]) {
+          rebuild_layout(c);
+          if (c.g.leader()) acc.z->st[S_LAYOUT] += 1;
+        }
+        TICK(2);
+        const int32_t tn = t + 1;
+        const bool next_b1 = tn < t0 + n_slots && (P.SPS == 1 || tn % P.SPS == 0);
+        if (threadIdx.x < 32) {
+          if (total > 0 && c.g.leader()) b3b(c, total);
+          __syncwarp();
+          if (next_b1)                       // B3b's live counts are final for the B1 shares
+            asm volatile("bar.arrive 3, %0;" :: "r"((int)blockDim.x) : "memory");
+          if (pass) placement_pass<true>(c, red, ph, t, acc);
+          if (c.g.leader()) {        // after the pass: this slot's active set
+            const long long na = v.h[H_NACT];
+            acc.z->act += na;
+            acc.z->memu += na * P.M - v.h[H_SUMU];
+            acc.z->rows += P.G;
+            acc.z->maxa = na > acc.z->maxa ? na : acc.z->maxa;
+            acc.z->st[S_SLOT] += 1;
+          }
+          TICK(3);
+          if (next_b1) {
+            asm volatile("bar.sync 2, %0;" :: "r"((int)blockDim.x) : "memory");   // P0(t) done
+            b1_share<0>(c, tn);
+          }
+          TICK(4);
+        } else {
+          Scn cw = c;
+          cw.g.off = 32;
+          const int nb = (int)blockDim.x - 32;
+#ifdef DILU_PHASE_TIMING
+          long long w0 = clock64(), w1;   // worker arm, first worker thread: st[19..21]
+          const long long w_arm0 = w0;
+#define WTICK(k) do { w1 = clock64(); if (threadIdx.x == 32) acc.z->st[k] += w1 - w0; w0 = w1; } while (0)
+#else
+#define WTICK(k) do { } while (0)
+#endif
+          phase0<false>(cw, t, acc);
+          asm volatile("bar.sync 1, %0;" :: "r"(nb) : "memory");   // every P0(t) fold done
+          WTICK(19);
+          if (next_b1) {
+            asm volatile("bar.arrive 2, %0;" :: "r"((int)blockDim.x) : "memory");   // for warp 0's share
+            asm volatile("bar.sync 3, %0;" :: "r"((int)blockDim.x) : "memory");     // B3b done
+            b1_share<1>(c, tn);              // c: the thread's fixed B1 range
+          }
+          phase1<false>(cw, t, acc);
+          asm volatile("bar.sync 1, %0;" :: "r"(nb) : "memory");
+          WTICK(20);
+          phase2<false>(cw, t, acc);
+          WTICK(21);
+#ifdef DILU_PHASE_TIMING
+          {   // st[23]: per slot, the slowest worker's finish (since the arm start) via shared max
+            const long long mine = clock64() - w_arm0;
+            atomicMax(reinterpret_cast<unsigned long long*>(&acc.z->st[22]), (unsigned long long)mine);
+          }
+#endif
+#undef WTICK
+        }
+        __syncthreads();     // join
+#ifdef DILU_PHASE_TIMING
+        if (c.g.leader()) { acc.z->st[23] += acc.z->st[22]; acc.z->st[22] = 0; }
+#endif
+        TICK(5);
+        continue;
+      }
       if (ovl) {
         bool pass = false;
         TICK(0);
-        if (t % P.SPS == 0) {
+        if (P.SPS == 1 || t % P.SPS == 0) {
           pass = boundary(c, red, ph, t, acc, true);   // B1 + B3 (+ barrier)
           if (v.h[H_ERR]) break;                                  // uniform after B3's barrier
         }
@@ -1964,6 +2136,7 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
           const int nb = (int)blockDim.x - 32;
 #ifdef DILU_PHASE_TIMING
           long long w0 = clock64(), w1;   // worker arm, first worker thread: st[19..21]
+          const long long w_arm0 = w0;
 #define WTICK(k) do { w1 = clock64(); if (threadIdx.x == 32) acc.z->st[k] += w1 - w0; w0 = w1; } while (0)
 #else
 #define WTICK(k) do { } while (0)
@@ -1976,13 +2149,22 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
           WTICK(20);
           phase2<false>(cw, t, acc);
           WTICK(21);
+#ifdef DILU_PHASE_TIMING
+          {
+            const long long mine = clock64() - w_arm0;
+            atomicMax(reinterpret_cast<unsigned long long*>(&acc.z->st[22]), (unsigned long long)mine);
+          }
+#endif
 #undef WTICK
         }
         __syncthreads();     // join: B1(t+1) resets the window fields P0(t) accumulates
-        TICK(4);
+#ifdef DILU_PHASE_TIMING
+        if (c.g.leader()) { acc.z->st[23] += acc.z->st[22]; acc.z->st[22] = 0; }
+#endif
+        TICK(5);
         continue;
       }
-      if (t % P.SPS == 0) {
+      if (P.SPS == 1 || t % P.SPS == 0) {
         // no barrier here: B1 touches only the per-function window fields, which P2(t-1)
         // never reads, and B1's own count barrier orders P2(t-1) before B3 mutates state
         TICK(0);
@@ -2035,7 +2217,7 @@ static __device__ void run_scenario(const Params& P, Red& red, View& sv, uint8_t
       if (alg2) {
         const int par = t & 1;
         const bool one = P.SPS == 1;         // buffers as in phase1
-        phase1_alg2<lat>(c, t, 1, v.iR + (one ? 0 : par) * P.I, 0, one ? v.iR + P.I : v.iBmin + par * P.I, 0,
+        phase1_alg2<lat>(c, t, 1, v.iR + (one ? 0 : par) * P.I, 0, one ? GP32(v.iR + P.I) : GP32(v.iBmin + par * P.I), 0,
                          v.fGang + par * P.F, 0,
                          v.iEmax + par * P.I, acc);
       } else {
@@ -2121,22 +2303,20 @@ constexpr int SMEM_MAX_THREADS = DILU_SMEM_THREADS;   // shared-memory variant: 
 
 template <bool SMEM, int VAR>
 __global__ void __launch_bounds__(SMEM ? SMEM_MAX_THREADS : 1024, SMEM ? DILU_MINB : 1)
-k_run(Params Pin, int32_t* next_scn, int32_t t0,
+k_run(const __grid_constant__ Params Pin, int32_t* next_scn, int32_t t0,
                                               int32_t n_slots, int32_t n_req,
                                               const int32_t* req_scn, const int32_t* req_func,
                                               int32_t* out_gpu, int32_t* out_iid) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ Red red;
-  __shared__ Params sP;
   __shared__ View sv;
-  if (threadIdx.x == 0) sP = Pin;
   for (;;) {
     if (threadIdx.x == 0) red.flag[0] = atomicAdd(next_scn, 1);
     __syncthreads();
     const int32_t sc = red.flag[0];
     __syncthreads();
-    if (sc >= sP.S) break;
-    run_scenario<SMEM, VAR>(sP, red, sv, smem, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu, out_iid);
+    if (sc >= Pin.S) break;
+    run_scenario<SMEM, VAR>(Pin, red, &sv, smem, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu, out_iid);
   }
 }
 
@@ -2145,28 +2325,26 @@ k_run(Params Pin, int32_t* next_scn, int32_t t0,
 // run in waves.  Same device code as k_run through the group abstraction.
 template <int VAR>
 __global__ void __launch_bounds__(1024, 1)
-k_run_cluster(Params Pin, int32_t t0, int32_t n_slots, int32_t n_req, const int32_t* req_scn,
+k_run_cluster(const __grid_constant__ Params Pin, int32_t t0, int32_t n_slots, int32_t n_req, const int32_t* req_scn,
               const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid) {
   __shared__ Red red;
-  __shared__ Params sP;
   __shared__ View sv;
   unsigned int crank, csize;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
-  if (threadIdx.x == 0) sP = Pin;
-  __syncthreads();
   const int32_t sc = blockIdx.x / csize;
-  if (sc >= sP.S) return;   // whole clusters only: uniform across the cluster
-  run_scenario<false, VAR>(sP, red, sv, nullptr, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu,
+  if (sc >= Pin.S) return;   // whole clusters only: uniform across the cluster
+  run_scenario<false, VAR>(Pin, red, &sv, nullptr, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu,
                       out_iid, (int)csize, (int)crank);
 }
 
 #ifndef DILU_VARIANT_TU   // the init / snapshot kernels live in dilu_api.cu's unit only
 // Initialise every scenario's block at slot 0 (one CTA per scenario).
+template <bool N>
 __global__ void k_init(Params P) {
   const int32_t sc = blockIdx.x;
   uint8_t* b = P.state + (size_t)sc * P.L.bytes;
-  View v = make_view(b, b, P.L);
+  const ViewT<N> v = make_view<N>(b, b, P.L);
   const int32_t* rows = P.funcs + (size_t)sc * P.F * 16;
   // (dilu_sim_reset zeroes the whole state area first: alignment gaps are defined bytes
   // when the run kernel stages the hot region -- compute-sanitizer initcheck clean)
@@ -2235,7 +2413,7 @@ __global__ void k_init(Params P) {
     v.h[H_NDEF] = nd;
   }
   for (int32_t q = threadIdx.x; q < P.I; q += blockDim.x) {
-    v.qFunc[q] = 0; v.qFirst[q] = 0; v.qN[q] = 0; v.qFail[q] = -1;
+    v.qN[q] = 0; v.qFail[q] = -1; v.qSlot[q] = 0;
   }
   for (int k = threadIdx.x; k < NT; k += blockDim.x) P.tally[(size_t)sc * NT + k] = 0;
   for (int k = threadIdx.x; k < NSTAT; k += blockDim.x) P.stats[(size_t)sc * NSTAT + k] = 0;
@@ -2243,9 +2421,10 @@ __global__ void k_init(Params P) {
 }
 
 // Snapshot for parity tests (off the timed path).
+template <bool N>
 __global__ void k_snapshot(Params P, int32_t id_cap, int32_t* out_gpu, int32_t* out_inst) {
   const int32_t sc = blockIdx.x;
-  View v = make_view(P.state + (size_t)sc * P.L.bytes, P.state + (size_t)sc * P.L.bytes, P.L);
+  const ViewT<N> v = make_view<N>(P.state + (size_t)sc * P.L.bytes, P.state + (size_t)sc * P.L.bytes, P.L);
   if (out_gpu)
     for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
       int32_t* o = out_gpu + ((size_t)sc * P.G + g) * 4;

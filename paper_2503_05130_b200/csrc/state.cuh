@@ -32,7 +32,8 @@ enum : int {
   H_NEV, H_CCNT = 10 /*6*/, H_CBASE = 16 /*7*/, H_GBASE = 23 /*6*/, H_CCNT2 = 29 /*6*/,
   H_RLN = 35 /* release-log entries appended */, H_NINF = 36, H_NDEF = 37,
   H_QLIVE = 38 /* live queue requests */, H_LASTEP = 39 /* release epoch at the last pass's end */,
-  H_QNEWPOS = 40 /* first request enqueued since the last pass, -1 if none */, H_WORDS = 44
+  H_QNEWPOS = 40 /* first request enqueued since the last pass, -1 if none */,
+  H_PNEV = 41 /* pipelined slots: events of the next boundary (b1_warp) */, H_WORDS = 44
 };
 
 // tally indices (match include/dilu.h)
@@ -41,9 +42,26 @@ enum : int {
   T_COLD, T_SOUT, T_SIN, T_SPLIT, T_HASH, T_ROWS, T_MAXA
 };
 
+// Element types of the state arrays.  Wide (ET<false>): int32 everywhere -- the cluster
+// engine and the global-memory CTA kernels.  Narrow (ET<true>): the shared-memory CTA
+// kernels when I, F, G <= 32767 and W <= 127: slot / function / GPU indices in int16,
+// flags, small counts and window counters in int8 -- the hot region of a C4 scenario
+// shrinks so more scenarios are resident per SM (DESIGN.md s5 "Narrow state").
+template <bool B, class A, class C> struct Sel { typedef A T; };
+template <class A, class C> struct Sel<false, A, C> { typedef C T; };
+template <bool N> struct ET {
+  typedef typename Sel<N, int16_t, int32_t>::T idx;    // slot, function, GPU index (or -1)
+  typedef typename Sel<N, int8_t, int32_t>::T small;   // flags, metas, counts <= 127
+  typedef typename Sel<N, int16_t, int32_t>::T quota;  // per-mille quotas, live counts
+};
+inline bool narrow_ok(int32_t G, int32_t F, int32_t I, int32_t W) {
+  return G <= 32767 && F <= 32767 && I <= 32767 && W <= 127;
+}
+
 struct Layout {
   int32_t G, F, I, W, B;   // B: slots per fused batch between second boundaries (1 = unfused)
   int32_t A2, LT;          // literal Alg.2 / request-level latency arrays present
+  int32_t N;               // narrow element types (ET<true>): CTA engine, hot region in smem
   // byte offsets inside one block
   size_t hdr;
   size_t gR, gL, gU, gN, gNs, gRes, gExcl, gGrow, gMask, gRel, rlG, rlE;
@@ -52,7 +70,7 @@ struct Layout {
       fPhase, fCap1;
   size_t fReg, fNsamp, fAcc, fHead, fUp, fDown, fThrn, fOld, fPv, fNlive, fLh, fLt, fGang, fFlag, fK,
       fList, fArr, fDep, fPidx, fInfL, fDefL;
-  size_t qFunc, qFirst, qN, qFail, qSlot, iQ;
+  size_t qN, qFail, qSlot, iQ;
   size_t rB, bB, gB;       // per-batch-slot r, LLM stage minimum, training gang (B > 1 only)
   size_t aTc, aTm, aRl, aLe, aSt, aOw, aDt;   // literal Alg.2 state (cfg.flags bit2 only)
   size_t fSlo, iEmax, eB;  // request-level latency (cfg.flags bit3 only)
@@ -62,47 +80,54 @@ struct Layout {
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B = 1,
-                          bool alg2 = false, bool lat = false) {
+                          bool alg2 = false, bool lat = false, bool narrow = false) {
   Layout L;
-  L.G = G; L.F = F; L.I = I; L.W = W; L.B = B; L.A2 = alg2; L.LT = lat;
+  L.G = G; L.F = F; L.I = I; L.W = W; L.B = B; L.A2 = alg2; L.LT = lat; L.N = narrow;
+  const size_t X = narrow ? 2 : 4;      // index arrays
+  const size_t S1 = narrow ? 1 : 4;     // small arrays
+  const size_t Q = narrow ? 2 : 4;      // quota / count arrays
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t at = o; o = align16(o + bytes); return at; };
   // hot region: touched every slot -> staged in shared memory when it fits
   L.hdr = take(H_WORDS * 4);
   L.gR = take(4 * (size_t)G); L.gL = take(4 * (size_t)G); L.gU = take(4 * (size_t)G);
-  L.gN = take(4 * (size_t)G);
-  L.gNs = take(4 * (size_t)G);          // row sizes at the last repack (overlapped slots, s5)
-  L.gRes = take(4 * (size_t)G * RES);
-  L.gExcl = take(4 * (size_t)G); L.gGrow = take(4 * (size_t)G);
+  L.gN = take(S1 * (size_t)G);
+  L.gNs = take(S1 * (size_t)G);         // row sizes at the last repack (overlapped slots, s5)
+  L.gRes = take(X * (size_t)G * RES);
+  L.gExcl = take(S1 * (size_t)G); L.gGrow = take(X * (size_t)G);
   L.gMask = take(8 * (size_t)G);        // bit (affinity_class & 63) per resident class
   L.rlG = take(4 * RLOG); L.rlE = take(4 * RLOG);
-  L.iId = take(4 * (size_t)I); L.iFunc = take(4 * (size_t)I); L.iMeta = take(4 * (size_t)I);
-  L.iReady = take(4 * (size_t)I); L.iNext = take(4 * (size_t)I); L.iR = take(4 * 2 * (size_t)I);
+  L.iId = take(4 * (size_t)I); L.iFunc = take(X * (size_t)I); L.iMeta = take(S1 * (size_t)I);
+  L.iReady = take(4 * (size_t)I); L.iNext = take(X * (size_t)I); L.iR = take(4 * 2 * (size_t)I);
 #ifdef DILU_HOT_PAD
   take(DILU_HOT_PAD);                   // layout-sensitivity parity variant
 #endif
-  L.fKind = take(4 * (size_t)F); L.fReq = take(4 * (size_t)F); L.fLim = take(4 * (size_t)F);
-  L.fMem = take(4 * (size_t)F); L.fCb = take(4 * (size_t)F); L.fIbs = take(4 * (size_t)F);
-  L.fNw = take(4 * (size_t)F); L.fCls = take(4 * (size_t)F); L.fDtr = take(4 * (size_t)F);
-  L.fPat = take(4 * (size_t)F); L.fScale = take(4 * (size_t)F); L.fPhase = take(4 * (size_t)F);
+  L.fKind = take(S1 * (size_t)F); L.fReq = take(Q * (size_t)F); L.fLim = take(Q * (size_t)F);
+  L.fCb = take(4 * (size_t)F); L.fIbs = take(4 * (size_t)F);
+  L.fNw = take(S1 * (size_t)F); L.fCls = take(4 * (size_t)F); L.fDtr = take(4 * (size_t)F);
+  L.fPat = take(4 * (size_t)F); L.fScale = take(4 * (size_t)F);
   L.fCap1 = take(8 * (size_t)F);
-  L.fReg = take(4 * (size_t)F); L.fNsamp = take(4 * (size_t)F); L.fAcc = take(4 * (size_t)F);
-  L.fHead = take(4 * (size_t)F); L.fUp = take(4 * (size_t)F); L.fDown = take(4 * (size_t)F);
-  L.fThrn = take(4 * (size_t)F);
+  L.fReg = take(S1 * (size_t)F); L.fNsamp = take(S1 * (size_t)F); L.fAcc = take(4 * (size_t)F);
+  L.fHead = take(S1 * (size_t)F); L.fUp = take(S1 * (size_t)F); L.fDown = take(S1 * (size_t)F);
+  L.fThrn = take(Q * (size_t)F);
   L.fOld = take(4 * (size_t)F); L.fPv = take(4 * (size_t)F);   // cp.async landing slots
-  L.fNlive = take(4 * (size_t)F); L.fLh = take(4 * (size_t)F);
-  L.fGang = take(4 * 2 * (size_t)F); L.fFlag = take(4 * (size_t)F);
+  L.fNlive = take(Q * (size_t)F); L.fLh = take(X * (size_t)F);
+  L.fGang = take(4 * 2 * (size_t)F); L.fFlag = take(S1 * (size_t)F);
   L.fArr = take(4 * (size_t)F); L.fDep = take(4 * (size_t)F); L.fPidx = take(4 * (size_t)F);
-  L.fInfL = take(4 * (size_t)F); L.fDefL = take(4 * (size_t)F);
+  L.fInfL = take(X * (size_t)F); L.fDefL = take(X * (size_t)F);
   // serial-path structures the leader walks every boundary (queue, free stack, ...)
   L.gRel = take(4 * (size_t)G);
-  L.fLt = take(4 * (size_t)F); L.fK = take(4 * (size_t)F); L.fList = take(4 * (size_t)F);
-  L.fstack = take(4 * (size_t)I);
-  L.fPrio = take(4 * (size_t)F); L.fCold = take(4 * (size_t)F);
-  L.qFunc = take(4 * (size_t)I); L.qFirst = take(4 * (size_t)I); L.qN = take(4 * (size_t)I);
-  L.qFail = take(4 * (size_t)I); L.qSlot = take(4 * (size_t)I); L.iQ = take(4 * (size_t)I);
+  L.fLt = take(X * (size_t)F); L.fK = take(4 * (size_t)F); L.fList = take(X * (size_t)F);
+  L.fstack = take(X * (size_t)I);
+  L.fPrio = take(S1 * (size_t)F);
+  // queue of pending requests: first member's slot (its function and first id are that
+  // instance's), member count, failure epoch; per instance its request index
+  L.qN = take(S1 * (size_t)I); L.qFail = take(4 * (size_t)I); L.qSlot = take(X * (size_t)I);
+  L.iQ = take(X * (size_t)I);
   L.hot_bytes = align16(o);
-  // cold region: stage placements and LLM stage minima -> stays in HBM/L2
+  // cold region: stage placements and LLM stage minima, per-function constants read only
+  // by placement / registration -> stays in HBM/L2 (L1-cached)
+  L.fMem = take(4 * (size_t)F); L.fCold = take(4 * (size_t)F); L.fPhase = take(4 * (size_t)F);
   L.iG = take(2 * (size_t)I * MAXST);   // int16 stage GPUs (G <= 32767)
   L.iSh0 = take(4 * (size_t)I);         // stage-0 memory share
   L.iShare = take(4 * (size_t)I * MAXST);
@@ -151,75 +176,138 @@ template <class T> struct Chk {
   __host__ __device__ operator T*() const { return b + o; }
 };
 #define VP(T) ::dilu::Chk<T>
+#define HP(T) ::dilu::Chk<T>
 #define DP(T) ::dilu::Chk<T>
 #define DPN(T) ::dilu::Chk<T>
 #else
 #define VP(T) T*
 #define DP(T) T* __restrict__
 #define DPN(T) T*
+#ifndef DILU_VMODE
+#define DILU_VMODE 1
+#endif
+#if defined(__CUDACC__) && defined(DILU_HOT_SMEM) && DILU_HOT_SMEM && DILU_VMODE != 1
+// Hot-region arrays of the shared-memory kernels (run_variants.cu units compiled with
+// DILU_HOT_SMEM=1): a 32-bit byte offset into the kernel's dynamic shared memory.  Every
+// access forms its address from the __shared__ symbol itself, so NVVM's address-space
+// inference emits LDS/STS/ATOMS (28 vs 33 cycles per dependent load against generic
+// LD/ST, tools/ubench/smem_chase.cu) with no __builtin_assume (whose false assumptions
+// would be undefined behaviour the optimiser may exploit) and half-size view fields.
+extern __shared__ __align__(16) uint8_t dilu_dsmem[];
+template <class T> struct SPtr {
+  uint32_t o;
+  SPtr() = default;
+  static __host__ __device__ SPtr at(size_t off) { SPtr r; r.o = (uint32_t)off; return r; }
+  __device__ __forceinline__ T* ptr() const { return reinterpret_cast<T*>(dilu_dsmem + o); }
+  template <class Ix> __device__ __forceinline__ T& operator[](Ix i) const { return ptr()[i]; }
+  template <class Ix> __device__ __forceinline__ SPtr operator+(Ix k) const {
+    return at(o + (size_t)(long long)k * sizeof(T));
+  }
+  __device__ __forceinline__ operator T*() const { return ptr(); }
+};
+#define HP(T) ::dilu::SPtr<T>
+#else
+#define HP(T) T*
+#endif
 #endif
 
 // Typed view of one scenario's block (pointers into smem or global).
-struct View {
-  typedef VP(int32_t) PI;
-  PI h;
-  PI gR, gL, gU, gN, gNs, gRes, gExcl, gGrow, gRel, rlG, rlE;
-  VP(unsigned long long) gMask;
-  PI iId, iFunc, iMeta, iReady, iSh0, iShare, iNext, iR, iBmin, fstack;
+template <bool N> struct ViewT {
+  typedef typename ET<N>::idx X;
+  typedef typename ET<N>::small S1;
+  typedef typename ET<N>::quota Q;
+  typedef VP(int32_t) PI;   // cold region / global arrays
+  typedef HP(int32_t) HI;   // hot region (shared memory in the DILU_HOT_SMEM kernels)
+  typedef HP(X) HX;
+  typedef HP(S1) HS;
+  typedef HP(Q) HQ;
+  HI h;
+  HI gR, gL, gU, gRel, rlG, rlE;
+  HS gN, gNs, gExcl;
+  HX gRes, gGrow;
+  HP(unsigned long long) gMask;
+  HI iId, iReady, iR;
+  HX iFunc, iNext, fstack;
+  HS iMeta;
+  PI iSh0, iShare, iBmin;
   VP(int16_t) iG;
-  PI fKind, fPrio, fReq, fLim, fMem, fCb, fIbs, fNw, fCold, fCls, fDtr, fPat,
-      fScale, fPhase;
-  VP(int64_t) fCap1;
-  PI fReg, fNsamp, fAcc, fHead, fUp, fDown, fThrn, fOld, fPv, fNlive, fLh, fLt, fGang,
-      fFlag, fK, fList, fArr, fDep, fPidx, fInfL, fDefL;
-  PI qFunc, qFirst, qN, qFail, qSlot, iQ;
+  HS fKind, fPrio, fNw;
+  HQ fReq, fLim;
+  HI fCb, fIbs, fCls, fDtr, fPat, fScale;
+  PI fMem, fCold, fPhase;
+  HP(int64_t) fCap1;
+  HS fReg, fNsamp, fHead, fUp, fDown, fFlag;
+  HQ fThrn, fNlive;
+  HI fAcc, fOld, fPv, fGang, fK, fArr, fDep, fPidx;
+  HX fLh, fLt, fList, fInfL, fDefL;
+  HS qN;
+  HI qFail;
+  HX qSlot, iQ;
   PI rB, bB, gB;
   PI aTc, aTm, aRl, aLe, aSt, aOw, aDt;
   PI fSlo, iEmax, eB;
   PI ring;  // global [F][W]
 };
 
+#if defined(__CUDACC__) && defined(DILU_HOT_SMEM) && DILU_HOT_SMEM && !defined(DILU_BOUNDS) && DILU_VMODE != 1
+template <class T> __host__ __device__ inline void dilu_set(SPtr<T>& f, uint8_t*, uint8_t*, size_t off, size_t) {
+  f = SPtr<T>::at(off);   // hot arrays always precede hot_bytes (make_layout)
+}
+template <class T> __host__ __device__ inline void dilu_set(T*& f, uint8_t* hot, uint8_t* b, size_t off, size_t hb) {
+  f = reinterpret_cast<T*>((off < hb ? hot : b) + off);
+}
+#endif
+template <bool N>
 #ifdef __CUDACC__
 __host__ __device__
 #endif
-inline View make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
+inline ViewT<N> make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
   // arrays in the hot region resolve against `hot` (smem copy or b), the rest against b
-  View v;
+  typedef typename ET<N>::idx X;
+  typedef typename ET<N>::small S1;
+  typedef typename ET<N>::quota Q;
+  ViewT<N> v;
   const long long G = L.G, F = L.F, I = L.I, BB = L.B > 1 ? L.B : 0;
   const long long AI = L.A2 ? I * MAXST : 0, AG = L.A2 ? G : 0;
 #ifdef DILU_BOUNDS
   int id = 0;
 #define PT(T, name, cnt) v.name = Chk<T>(reinterpret_cast<T*>((L.name < L.hot_bytes ? hot : b) + L.name), (cnt), id++)
+#elif defined(__CUDACC__) && defined(DILU_HOT_SMEM) && DILU_HOT_SMEM && DILU_VMODE != 1
+  // shared-memory kernels: hot arrays are offsets into dynamic shared memory (SPtr), the
+  // cold ones generic pointers into the global block
+#define PT(T, name, cnt) dilu_set(v.name, hot, b, L.name, L.hot_bytes)
 #else
 #define PT(T, name, cnt) v.name = reinterpret_cast<T*>((L.name < L.hot_bytes ? hot : b) + L.name)
 #endif
   // (order = DILU_ARRAY_NAMES below)
 #ifdef DILU_BOUNDS
   v.h = Chk<int32_t>(reinterpret_cast<int32_t*>(hot + L.hdr), H_WORDS, id++);
+#elif defined(__CUDACC__) && defined(DILU_HOT_SMEM) && DILU_HOT_SMEM && DILU_VMODE != 1
+  v.h = SPtr<int32_t>::at(L.hdr);
 #else
   v.h = reinterpret_cast<int32_t*>(hot + L.hdr);
 #endif
-  PT(int32_t, gR, G); PT(int32_t, gL, G); PT(int32_t, gU, G); PT(int32_t, gN, G); PT(int32_t, gNs, G);
-  PT(int32_t, gRes, G * RES); PT(int32_t, gExcl, G); PT(int32_t, gGrow, G); PT(int32_t, gRel, G);
+  PT(int32_t, gR, G); PT(int32_t, gL, G); PT(int32_t, gU, G); PT(S1, gN, G); PT(S1, gNs, G);
+  PT(X, gRes, G * RES); PT(S1, gExcl, G); PT(X, gGrow, G); PT(int32_t, gRel, G);
   PT(int32_t, rlG, RLOG); PT(int32_t, rlE, RLOG);
   PT(unsigned long long, gMask, G);
-  PT(int32_t, iId, I); PT(int32_t, iFunc, I); PT(int32_t, iMeta, I); PT(int32_t, iReady, I);
-  PT(int32_t, iSh0, I); PT(int32_t, iShare, I * MAXST); PT(int32_t, iNext, I); PT(int32_t, iR, 2 * I);
-  PT(int32_t, iBmin, 2 * I); PT(int32_t, fstack, I);
+  PT(int32_t, iId, I); PT(X, iFunc, I); PT(S1, iMeta, I); PT(int32_t, iReady, I);
+  PT(int32_t, iSh0, I); PT(int32_t, iShare, I * MAXST); PT(X, iNext, I); PT(int32_t, iR, 2 * I);
+  PT(int32_t, iBmin, 2 * I); PT(X, fstack, I);
   PT(int16_t, iG, I * MAXST);
-  PT(int32_t, fKind, F); PT(int32_t, fPrio, F); PT(int32_t, fReq, F); PT(int32_t, fLim, F);
-  PT(int32_t, fMem, F); PT(int32_t, fCb, F); PT(int32_t, fIbs, F); PT(int32_t, fNw, F);
+  PT(S1, fKind, F); PT(S1, fPrio, F); PT(Q, fReq, F); PT(Q, fLim, F);
+  PT(int32_t, fMem, F); PT(int32_t, fCb, F); PT(int32_t, fIbs, F); PT(S1, fNw, F);
   PT(int32_t, fCold, F); PT(int32_t, fCls, F); PT(int32_t, fDtr, F); PT(int32_t, fPat, F);
   PT(int32_t, fScale, F); PT(int32_t, fPhase, F);
   PT(int64_t, fCap1, F);
-  PT(int32_t, fReg, F); PT(int32_t, fNsamp, F); PT(int32_t, fAcc, F); PT(int32_t, fHead, F);
-  PT(int32_t, fUp, F); PT(int32_t, fDown, F); PT(int32_t, fThrn, F); PT(int32_t, fOld, F);
-  PT(int32_t, fPv, F); PT(int32_t, fNlive, F); PT(int32_t, fLh, F); PT(int32_t, fLt, F);
-  PT(int32_t, fGang, 2 * F); PT(int32_t, fFlag, F); PT(int32_t, fK, F); PT(int32_t, fList, F);
-  PT(int32_t, fArr, F); PT(int32_t, fDep, F); PT(int32_t, fPidx, F); PT(int32_t, fInfL, F);
-  PT(int32_t, fDefL, F);
-  PT(int32_t, qFunc, I); PT(int32_t, qFirst, I); PT(int32_t, qN, I); PT(int32_t, qFail, I);
-  PT(int32_t, qSlot, I); PT(int32_t, iQ, I);
+  PT(S1, fReg, F); PT(S1, fNsamp, F); PT(int32_t, fAcc, F); PT(S1, fHead, F);
+  PT(S1, fUp, F); PT(S1, fDown, F); PT(Q, fThrn, F); PT(int32_t, fOld, F);
+  PT(int32_t, fPv, F); PT(Q, fNlive, F); PT(X, fLh, F); PT(X, fLt, F);
+  PT(int32_t, fGang, 2 * F); PT(S1, fFlag, F); PT(int32_t, fK, F); PT(X, fList, F);
+  PT(int32_t, fArr, F); PT(int32_t, fDep, F); PT(int32_t, fPidx, F); PT(X, fInfL, F);
+  PT(X, fDefL, F);
+  PT(S1, qN, I); PT(int32_t, qFail, I);
+  PT(X, qSlot, I); PT(X, iQ, I);
   PT(int32_t, rB, BB * I); PT(int32_t, bB, BB * I); PT(int32_t, gB, BB * F);
   PT(int32_t, aTc, AI); PT(int32_t, aTm, AI); PT(int32_t, aRl, AI); PT(int32_t, aLe, AI);
   PT(int32_t, aSt, AG); PT(int32_t, aOw, AG); PT(int32_t, aDt, AG);
@@ -241,7 +329,7 @@ inline View make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
   "fKind", "fPrio", "fReq", "fLim", "fMem", "fCb", "fIbs", "fNw", "fCold", "fCls", "fDtr",     \
   "fPat", "fScale", "fPhase", "fCap1", "fReg", "fNsamp", "fAcc", "fHead", "fUp", "fDown",      \
   "fThrn", "fOld", "fPv", "fNlive", "fLh", "fLt", "fGang", "fFlag", "fK", "fList", "fArr",     \
-  "fDep", "fPidx", "fInfL", "fDefL", "qFunc", "qFirst", "qN", "qFail", "qSlot", "iQ", "rB",    \
+  "fDep", "fPidx", "fInfL", "fDefL", "qN", "qFail", "qSlot", "iQ", "rB",    \
   "bB", "gB", "aTc", "aTm", "aRl", "aLe", "aSt", "aOw", "aDt", "fSlo", "iEmax", "eB", "ring",  \
   "members"
 

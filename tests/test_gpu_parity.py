@@ -95,13 +95,18 @@ def test_c4_sample_full_hour():
 
 
 @pytest.mark.parametrize("mode", ["cta_threads64", "cta_threads1024", "cta_no_smem", "cta_no_ovl",
-                                  "cluster_k1", "cluster_k3"])
+                                  "cta_pipe", "cta_pipe_threads96", "cluster_k1", "cluster_k3"])
 def test_launch_shape_invariance(mode, monkeypatch):
     """Both engines and several launch shapes give bit-identical results (45 scenarios)."""
     full = di.c4(n_scenarios=4096, T=600)
     wl = full.subset(np.arange(5, 4096, 91))
     engine, _, shape = mode.partition("_")
     monkeypatch.setenv("DILU_ENGINE", engine)
+    if shape.startswith("pipe"):     # pipelined overlapped slot (DILU_PIPE, DESIGN.md s5)
+        monkeypatch.setenv("DILU_PIPE", "1")
+        shape = shape[5:]
+    if shape == "threads96":
+        monkeypatch.setenv("DILU_THREADS", "96")
     if shape == "threads64":
         monkeypatch.setenv("DILU_THREADS", "64")
     elif shape == "threads1024":
@@ -474,3 +479,19 @@ def test_c5_timed_window_vs_frozen_oracle():
     per, tot = gs.metrics()
     assert np.array_equal(per.cpu().numpy(), np.array(gold["per_scenario"], dtype=np.int64))
     assert np.array_equal(tot.cpu().numpy(), np.array(gold["sum"], dtype=np.int64))
+
+
+def test_modes_directional_c4_slice():
+    """SURVEY s8(f) #1 directional claims on the GPU path (paper-level, absolute values
+    unpinned; Table 3): on the same C4 sweep points Dilu occupies no more GPU-slots
+    than StaticLimit (MPS-l) or Exclusive, and the lazy window starts no more instances cold
+    than eager (FaST-GS+-like) scaling."""
+    base = di.c4(n_scenarios=4096, T=900).subset(np.arange(9, 4096, 137))
+    tot = {}
+    for m in (0, 1, 2, 4):
+        gs = gpu_sim(di.with_modes(base, [m] * base.S))
+        gs.scale_step(900)
+        tot[m] = gs.metrics(per_scenario=False)[1].cpu().numpy()
+    act = {m: tot[m][T["gpu_slots_active"]] for m in tot}
+    assert act[0] <= act[2] and act[0] <= act[1], act
+    assert tot[0][T["cold_starts"]] <= tot[4][T["cold_starts"]]

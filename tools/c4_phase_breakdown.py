@@ -17,9 +17,16 @@ s0 = torch.cuda.Event(enable_timing=True); s1 = torch.cuda.Event(enable_timing=T
 s0.record(); sim.scale_step(slots); s1.record(); torch.cuda.synchronize()
 per = np.zeros((n, 24), dtype=np.int64)
 lib().dilu_kernel_stats(sim.h, per.ctypes.data, None)
+# timers 8..13 are the leader's TICK(0..5); in the pipelined (overlapped) C4 path:
+# 9 = prologue B1 + B3a + barrier, 10 = repack, 11 = B3b + placement pass + fold,
+# 12 = wait for P0 + B1 of the next boundary (warp 0), 13 = join wait;
+# 19..21 = the first worker thread's P0 / P1 / P2 (each incl. its barrier wait),
+# 23 = the slowest worker's finish since the arm start (summed per slot)
 names = ["attempts", "retry_checks", "row_repacks", "boundary_events", "queue_scans", "slots",
-         "resident_slots", "function_slots", "pre_boundary", "boundary", "repack", "p0", "p1", "p2",
-         "b3", "terminate", "enqueue", "next_attempt", "place", "w_p0", "w_p1", "w_p2", "b1_count_scan", "t23"]
+         "resident_slots", "function_slots", "tick0_pre", "tick1_b3a", "tick2_repack",
+         "tick3_ctl_place", "tick4_ctl_b1", "tick5_join",
+         "b3", "terminate", "enqueue", "next_attempt", "place", "w_p0", "w_p1", "w_p2", "scratch",
+         "worker_arm_max"]
 tot = per.sum(0)
 ss = tot[5]
 out = {"ms": s0.elapsed_time(s1), "scenario_slots": int(ss)}
