@@ -456,10 +456,7 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
     const char* e = getenv("DILU_NO_OVL");
     P.ovl = cold_ok && variant_of(cfg, s->L) == 0 && G <= WARP_PLACE_MAX && s->threads >= 64 &&
             !(e && atoi(e));
-    // DILU_PIPE=1: the pipelined overlapped slot (B1 shares after P0, B3 split around the
-    // control arm) -- exact, measured slower on C4, kept as a parity variant
-    const char* pe = getenv("DILU_PIPE");
-    if (P.ovl && pe && atoi(pe)) P.ovl = 2;
+
   }
   if (getenv("DILU_VERBOSE"))
     fprintf(stderr, "dilu: cta engine threads=%d smem=%d hot=%zu per_sm=%d grid=%d ovl=%d\n", s->threads,

@@ -313,6 +313,15 @@ template <int N> static __device__ __forceinline__ void cp_async_wait_group() {
 }
 
 
+// Serial helpers the leader / warp 0 call from several places (event application,
+// placement, rollback): one out-of-line copy each keeps the code the SM executes per
+// slot small -- with several resident scenarios per SM at different points of the slot,
+// inlined copies thrash the instruction cache (ncu "no_instruction" stalls).
+#ifndef DILU_SERIAL_INLINE
+#define DILU_SERIAL __forceinline__
+#else
+#define DILU_SERIAL __forceinline__
+#endif
 // ---- serial helpers (thread 0 only) ------------------------------------------------
 
 static __device__ void list_append(const View& v, int32_t f, int32_t s) {
@@ -322,8 +331,10 @@ static __device__ void list_append(const View& v, int32_t f, int32_t s) {
   if (v.fLt[f] < 0) v.fLh[f] = s; else v.iNext[v.fLt[f]] = s;
   v.fLt[f] = s;
 }
-static __device__ void list_remove(const View& v, int32_t f, int32_t s) {
+static __device__ DILU_SERIAL void list_remove(Scn& c, int32_t f, int32_t s) {
+  DILU_VIEW(v, c);
   int32_t prev = -1, cur = v.fLh[f];
+  #pragma unroll 1
   while (cur >= 0 && cur != s) { prev = cur; cur = v.iNext[cur]; }
   if (cur < 0) return;
   int32_t nx = v.iNext[cur];
@@ -336,7 +347,7 @@ static __device__ __forceinline__ long long res_key(const View& v, int32_t s) {
   return ((long long)v.fPrio[v.iFunc[s]] << 32) | (uint32_t)v.iId[s];
 }
 
-static __device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
+static __device__ DILU_SERIAL void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
   DILU_VIEW(v, c);
   const int32_t f = v.iFunc[s];
   if (v.gN[g] == 0) v.h[H_NACT] += 1;
@@ -349,6 +360,7 @@ static __device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
   int pos = v.gN[g];
   if (!c.P->ovl) {            // keep (prio, id) order now ...
     const long long k = res_key(v, s);
+    #pragma unroll 1
     while (pos > 0 && res_key(v, res[pos - 1]) > k) { res[pos] = res[pos - 1]; --pos; }
   }                           // ... or append (overlapped slots: rows below gNs never move
   res[pos] = s;               // while P1 reads them; the next repack sorts the row)
@@ -367,11 +379,12 @@ static __device__ void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
   v.h[H_DIRTY] = 1;
 }
 
-static __device__ void release(Scn& c, int32_t s) {
+static __device__ DILU_SERIAL void release(Scn& c, int32_t s) {
   DILU_VIEW(v, c);
   const int32_t f = v.iFunc[s];
   const int32_t meta = v.iMeta[s];
   const int n = nst_of(meta);
+  #pragma unroll 1
   for (int k = 0; k < n; ++k) {
     const int32_t g = v.iG[s * MAXST + k];
     const int32_t sh = k == 0 ? v.iSh0[s] : v.iShare[s * MAXST + k];
@@ -382,11 +395,14 @@ static __device__ void release(Scn& c, int32_t s) {
     const auto res = v.gRes + (size_t)g * RES;
     int j = 0;
     const int nr = v.gN[g];
+    #pragma unroll 1
     while (j < nr && res[j] != s) ++j;
+    #pragma unroll 1
     for (; j + 1 < nr; ++j) res[j] = res[j + 1];
     v.gN[g] = nr - 1;
     if (nr - 1 == 0) v.h[H_NACT] -= 1;
     unsigned long long m = 0;
+    #pragma unroll 1
     for (int x = 0; x < nr - 1; ++x) m |= 1ull << (v.fCls[v.iFunc[res[x]]] & 63);
     v.gMask[g] = m;
     v.iG[s * MAXST + k] = -1;
@@ -403,18 +419,19 @@ static __device__ void release(Scn& c, int32_t s) {
 #define TSTART do { } while (0)
 #define TSTOP(k) do { } while (0)
 #endif
-static __device__ void terminate_impl(Scn& c, int32_t s);
+static __device__ DILU_SERIAL void terminate_impl(Scn& c, int32_t s);
 static __device__ void terminate(Scn& c, int32_t s) {
   TSTART;
   terminate_impl(c, s);
   TSTOP(15);
 }
-static __device__ void terminate_impl(Scn& c, int32_t s) {
+static __device__ DILU_SERIAL void terminate_impl(Scn& c, int32_t s) {
   DILU_VIEW(v, c);
   const int32_t f = v.iFunc[s];
   if (st_of(v.iMeta[s]) == ST_PLACED) {
     const int32_t ep = ++v.h[H_EPOCH];   // room was freed: queued failures may now succeed
     const int ns = nst_of(v.iMeta[s]);
+    #pragma unroll 1
     for (int k = 0; k < ns; ++k) {
       const int32_t g = v.iG[s * MAXST + k];
 #ifdef DILU_TERM_PROBE
@@ -431,15 +448,17 @@ static __device__ void terminate_impl(Scn& c, int32_t s) {
     release(c, s);
   }
   v.iMeta[s] = ST_FREE;
-  list_remove(v, f, s);
+  list_remove(c, f, s);
   v.fNlive[f] -= 1;
   v.h[H_NLIVE] -= 1;
   v.fstack[v.h[H_FSTOP]++] = s;
 }
 
-static __device__ void compact_queue(const View& v) {
+static __device__ DILU_SERIAL void compact_queue(Scn& c) {
+  DILU_VIEW(v, c);
   const int32_t n = v.h[H_QLEN];
   int32_t k = 0;
+  #pragma unroll 1
   for (int32_t q = 0; q < n; ++q) {
     if (v.qN[q] == 0) continue;
     if (k != q) {
@@ -453,24 +472,25 @@ static __device__ void compact_queue(const View& v) {
 }
 
 // enqueue one request of n new instances of f; returns first id or -1 on capacity error
-static __device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n);
+static __device__ DILU_SERIAL int32_t enqueue_impl(Scn& c, int32_t f, int32_t n);
 static __device__ int32_t enqueue(Scn& c, int32_t f, int32_t n) {
   TSTART;
   const int32_t r = enqueue_impl(c, f, n);
   TSTOP(16);
   return r;
 }
-static __device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
+static __device__ DILU_SERIAL int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
   DILU_VIEW(v, c);
   if (v.h[H_FSTOP] < n) { v.h[H_ERR] = 6; return -1; }
   if (v.h[H_QLEN] == c.P->I) {
-    compact_queue(v);
+    compact_queue(c);
     v.h[H_QNEWPOS] = 0;               // positions moved: the next pass scans everything
   }
   const int32_t first = v.h[H_NEXT_IID];
   const int32_t q = v.h[H_QLEN]++;
   v.h[H_QLIVE] += 1;
   if (v.h[H_QNEWPOS] < 0) v.h[H_QNEWPOS] = q;
+  #pragma unroll 1
   for (int32_t j = 0; j < n; ++j) {
     const int32_t s = v.fstack[--v.h[H_FSTOP]];
     v.iId[s] = v.h[H_NEXT_IID]++;
@@ -479,6 +499,7 @@ static __device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
     v.iReady[s] = BIG;               // not ready until placed (read racily in overlapped slots)
     v.iQ[s] = q;                      // request index (single-instance kills are O(1))
     if (j == 0) v.qSlot[q] = s;
+    #pragma unroll 1
     for (int k = 0; k < MAXST; ++k) v.iG[s * MAXST + k] = -1;
     v.iBmin[s] = BIG;
     v.iBmin[c.P->I + s] = BIG;
@@ -491,7 +512,8 @@ static __device__ int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
   return first;
 }
 
-static __device__ void register_func(const View& v, int32_t f, int32_t t, int32_t Tp) {
+static __device__ DILU_SERIAL void register_func(Scn& c, int32_t f, int32_t t, int32_t Tp) {
+  DILU_VIEW(v, c);
   if (v.fReg[f]) return;
   v.fReg[f] = 1;
   v.fNsamp[f] = 0; v.fAcc[f] = 0; v.fHead[f] = 0; v.fUp[f] = 0; v.fDown[f] = 0;
@@ -500,8 +522,10 @@ static __device__ void register_func(const View& v, int32_t f, int32_t t, int32_
   v.fPidx[f] = (int32_t)(((long long)t + v.fPhase[f]) % Tp);   // arrivals index for slot t
 }
 
-static __device__ void kill_queue_entries_of(const View& v, int32_t f) {
+static __device__ DILU_SERIAL void kill_queue_entries_of(Scn& c, int32_t f) {
+  DILU_VIEW(v, c);
   const int32_t n = v.h[H_QLEN];
+  #pragma unroll 1
   for (int32_t q = 0; q < n; ++q)
     if (v.qN[q] > 0 && v.iFunc[v.qSlot[q]] == f) { v.qN[q] = 0; v.h[H_QLIVE] -= 1; }
 }
@@ -547,6 +571,7 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
   const long long aM = (long long)P.aw * P.M, bQ = (long long)P.bw * P.Q;
   const unsigned long long MASK40 = (1ull << 40) - 1;
   unsigned long long best = ~0ull;
+  #pragma unroll 1
   for (int32_t g = PG::rank(c); g < P.G; g += PG::size(c)) {
     if (v.gExcl[g]) continue;
     const int32_t n = v.gN[g];
@@ -562,6 +587,7 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
       // affinity: the class bitmask rules most GPUs out exactly; scan on a hit
       int aff = 0;
       if ((v.gMask[g] >> (cls & 63)) & 1ull)
+        #pragma unroll 1
         for (int j = 0; j < n && !aff; ++j) aff = (v.fCls[v.iFunc[res[j]]] == cls);
       const unsigned long long K = (unsigned long long)(aM * R + bQ * U);
       key = ((unsigned long long)(aff ? 0 : 1) << 62) | ((MASK40 - K) << 22) |
@@ -583,12 +609,15 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
     int k = 0;
     long long sum = 0;
     bool okk = false;
+    #pragma unroll 1
     for (int r = 0; r < P.max_stages; ++r) {
       unsigned long long kk = ~0ull;
+      #pragma unroll 1
       for (int32_t g = PG::rank(c); g < P.G; g += PG::size(c)) {
         const int32_t n = v.gN[g];
         if (n == 0 || v.gExcl[g] || n >= RES) continue;
         bool dup = false;
+        #pragma unroll 1
         for (int j = 0; j < r; ++j) dup |= (picked[j] == g);
         if (dup) continue;
         if (v.gR[g] + req > c.om || v.gL[g] + lim > c.ga) continue;
@@ -609,6 +638,7 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
     if (okk) {
       if (PG::leader(c)) {
         int32_t left = mem;
+        #pragma unroll 1
         for (int j = 0; j < k; ++j) {
           const int32_t sh = pfree[j] < left ? pfree[j] : left;
           commit(c, s, picked[j], sh);
@@ -643,15 +673,17 @@ static __device__ __forceinline__ bool could_help(const Scn& c, int32_t g, int32
 // Could any GPU released after epoch fe now host a request of f?  Walks the release
 // log back to fe (usually 1-3 entries); falls back to scanning every GPU's last-release
 // epoch when the log no longer covers fe.
-static __device__ bool hope_after(const Scn& c, int32_t fe, int32_t f) {
+static __device__ DILU_SERIAL bool hope_after(const Scn& c, int32_t fe, int32_t f) {
   DILU_CVIEW(v, c);
   const int32_t n = v.h[H_RLN];
   const int32_t lo = n > RLOG ? n - RLOG : 0;
   if (n > RLOG && v.rlE[lo % RLOG] > fe) {
+    #pragma unroll 1
     for (int32_t g = 0; g < c.P->G; ++g)
       if (v.gRel[g] > fe && could_help(c, g, f)) return true;
     return false;
   }
+  #pragma unroll 1
   for (int32_t k = n - 1; k >= lo; --k) {
     if (v.rlE[k % RLOG] <= fe) break;
     if (could_help(c, v.rlG[k % RLOG], f)) return true;
@@ -668,6 +700,7 @@ static __device__ int32_t next_attempt(Scn& c, int32_t q, int32_t qn, Acc& acc) 
   const int lane = threadIdx.x & 31;
   const int32_t ep = v.h[H_EPOCH];
   int32_t nfail = 0, found = qn, nhope = 0;
+  #pragma unroll 1
   for (int32_t p = q; p < qn; p += 32) {
     const int32_t qq = p + lane;
     int cls = 0;                      // 0 dead/none, 1 fails again, 2 needs an attempt
@@ -715,6 +748,7 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
   int32_t qn = 0;
   bool removed = false;                 // leader only
   int32_t q = 0, prev = -1, prev_placed = 0;
+  #pragma unroll 1
   for (;;) {
     // One warp-0 section per attempt: finish the previous request (leader), find the next
     // request needing a real attempt (warp 0, 32 entries per step), gather its members
@@ -722,17 +756,21 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
     TSTART;
     if (WARP || c.g.lead_warp()) {
       if (WARP && prev >= 0)                  // clear I* marks: every lane clears a stride
+        #pragma unroll 1
         for (int32_t g = threadIdx.x; g < c.P->G; g += 32) v.gExcl[g] = 0;   // (no iG loads)
       if (PG::leader(c) && prev >= 0) {
         const int32_t n = v.qN[prev], f = v.iFunc[v.qSlot[prev]];
         if (!WARP)
+          #pragma unroll 1
           for (int j = 0; j < prev_placed; ++j) {   // clear I* marks
             const int32_t s = c.members[j];
             const int ns = nst_of(v.iMeta[s]);
+            #pragma unroll 1
             for (int k = 0; k < ns; ++k) v.gExcl[v.iG[s * MAXST + k]] = 0;
           }
         if (prev_placed == n) {
           const int32_t cold = v.fCold[f];
+          #pragma unroll 1
           for (int j = 0; j < n; ++j) {
             const int32_t s = c.members[j];
             v.iMeta[s] = (v.iMeta[s] & ~3) | ST_PLACED;
@@ -745,6 +783,7 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
           v.h[H_QLIVE] -= 1;
           removed = true;
         } else {
+          #pragma unroll 1
           for (int j = 0; j < prev_placed; ++j) release(c, c.members[j]);  // rollback
           acc.z->pfail += 1;
           v.qFail[prev] = v.h[H_EPOCH];
@@ -770,6 +809,7 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
         if (e < qn) {                   // gang members, ascending id
           const int32_t n = v.qN[e], s0 = v.qSlot[e], f = v.iFunc[s0], first = v.iId[s0];
           int j = 0;
+          #pragma unroll 1
           for (int32_t s = v.fLh[f]; s >= 0 && j < n; s = v.iNext[s]) {
             const int32_t id = v.iId[s];
             if (id >= first && id < first + n) c.members[j++] = s;
@@ -787,6 +827,7 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
     int placed = 0;
     {
       TSTART;
+      #pragma unroll 1
       for (int j = 0; j < n; ++j) {
         if (!place_one<WARP>(c, red, ph, c.g.K == 1 ? c.members[j] : __ldcg(c.members + j))) break;
         ++placed;
@@ -798,7 +839,7 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
     ++q;
   }
   if (PG::leader(c)) {
-    if (removed) compact_queue(v);
+    if (removed) compact_queue(c);
     v.h[H_LASTEP] = v.h[H_EPOCH];
     v.h[H_QNEWPOS] = -1;
   }
@@ -826,16 +867,19 @@ static __device__ void rebuild_layout(Scn& c) {
   const Params& P = *c.P;
   if (c.g.crank == 0 && threadIdx.x < 6) { v.h[H_CCNT + threadIdx.x] = 0; v.h[H_CCNT2 + threadIdx.x] = 0; }
   c.g.sync();
+  #pragma unroll 1
   for (int32_t g = c.g.rank(); g < P.G; g += c.g.size()) {
     const int32_t n = v.gN[g];
     if (P.ovl && n > 1) {     // overlapped slots append commits: restore (prio, id) order
       const auto res = v.gRes + (size_t)g * RES;
       long long kp = res_key(v, res[0]);
+      #pragma unroll 1
       for (int j = 1; j < n; ++j) {
         const int32_t s = res[j];
         const long long k = res_key(v, s);
         if (k > kp) { kp = k; continue; }
         int pos = j;
+        #pragma unroll 1
         while (pos > 0 && res_key(v, res[pos - 1]) > k) { res[pos] = res[pos - 1]; --pos; }
         res[pos] = s;
       }
@@ -846,6 +890,7 @@ static __device__ void rebuild_layout(Scn& c) {
   c.g.sync();
   if (c.g.leader()) {
     int32_t cb = 0, gb = 0;
+    #pragma unroll 1
     for (int k = 0; k < 6; ++k) {
       v.h[H_CBASE + k] = cb;
       v.h[H_GBASE + k] = gb;
@@ -857,6 +902,7 @@ static __device__ void rebuild_layout(Scn& c) {
     v.h[H_DIRTY] = 0;
   }
   c.g.sync();
+  #pragma unroll 1
   for (int32_t g = c.g.rank(); g < P.G; g += c.g.size()) {
     const int32_t n = v.gN[g];
     if (n > 0) {
@@ -1709,111 +1755,6 @@ static __device__ int32_t b1_func(Scn& c, int32_t f, int32_t sec) {
   return ev;
 }
 
-// B1 share of one boundary (pipelined slots): every thread pushes and
-// decides its own contiguous function range [b1lo, b1hi) (the same range every call, so
-// the thread that issues a function's fOld prefetch is the one that consumes it).  Workers
-// run it right after P0 (ALLOW = 1: P0's fPv copies, the last committed group, may stay in
-// flight), warp 0 after its placement pass (ALLOW = 0).  Flags land in fFlag.
-template <int ALLOW>
-static __device__ void b1_share(Scn& c, int32_t t) {
-  const Params& P = *c.P;
-  const int32_t sec = P.SPS == 1 ? t : t / P.SPS;
-#if DILU_HOT_SMEM
-  cp_async_wait_group<ALLOW>();                    // this thread's last fOld copies landed
-#endif
-  for (int32_t f = c.b1lo; f < c.b1hi; ++f) b1_func(c, f, sec);
-#if DILU_HOT_SMEM
-  cp_async_commit();
-#endif
-}
-
-// Ordered event list of the boundary from fFlag (warp 0: one ballot per 32 functions);
-// returns the event count (uniform over the warp).
-static __device__ int32_t compact_events(Scn& c) {
-  DILU_VIEW(v, c);
-  const Params& P = *c.P;
-  const int lane = threadIdx.x & 31;
-  int32_t cnt = 0;
-  for (int32_t base = 0; base < P.F; base += 32) {
-    const int32_t f = base + lane;
-    const bool ev = f < P.F && v.fFlag[f] != 0;
-    const unsigned m = __ballot_sync(0xffffffffu, ev);
-    if (ev) v.fList[cnt + __popc(m & ((1u << lane) - 1))] = f;
-    cnt += __popc(m);
-  }
-  return cnt;
-}
-
-// ---- pipelined slots: B3 split around the control arm --------------------
-// B3a (leader, before the slot's barrier): the state-removing half of the boundary's events
-// in the paper's order -- departures (queue entries dropped, instances released), scale-in
-// victims -- plus the registration of arriving functions (P0 of this slot sees them) and the
-// capacity rule evaluated in the paper's order (live instances may not exceed max_instances
-// at any enqueue; D3).  The enqueues themselves (scale-outs, then arrivals, each
-// in function order: the ids the paper's order assigns) run in b3b inside the control arm,
-// where only pending (not warm) instances appear beside the running P0/P1/P2.
-static __device__ void b3a(Scn& c, int32_t t, int32_t total, Acc& acc) {
-  DILU_VIEW(v, c);
-  const Params& P = *c.P;
-  acc.z->st[S_EVENT] += total;
-  long long live = v.h[H_NLIVE];
-  for (int32_t e = 0; e < total; ++e) {          // step 2: departures
-    const int32_t f = v.fList[e];
-    if (!(v.fFlag[f] & EV_DEP)) continue;
-    live -= v.fNlive[f];
-    kill_queue_entries_of(v, f);
-    while (v.fLh[f] >= 0) terminate(c, v.fLh[f]);
-    v.fReg[f] = 0;
-  }
-  bool err = false;
-  for (int32_t e = 0; e < total && !err; ++e) {  // step 3: hscaler actions
-    const int32_t f = v.fList[e];
-    const int32_t ev = v.fFlag[f];
-    if (ev & EV_OUT) {
-      const int32_t k = v.fK[f];
-      for (int32_t j = 0; j < k && !err; ++j) { if (live + 1 > P.I) err = true; else live += 1; }
-      acc.z->sout += 1;
-    } else if (ev & EV_IN) {
-      const int32_t victim = v.fLt[f];           // highest live id (Q19)
-      if (st_of(v.iMeta[victim]) == ST_PEND) {   // its own request
-        v.qN[v.iQ[victim]] = 0;
-        v.h[H_QLIVE] -= 1;
-      }
-      terminate(c, victim);
-      live -= 1;
-      acc.z->sin += 1;
-    }
-  }
-  for (int32_t e = 0; e < total && !err; ++e) {  // step 4: arrivals (registration)
-    const int32_t f = v.fList[e];
-    if (!(v.fFlag[f] & EV_ARR)) continue;
-    register_func(v, f, t, P.Tp);
-    if (v.fKind[f] == K_TRAIN) {
-      if (live + v.fNw[f] > P.I) err = true; else live += v.fNw[f];
-    } else {
-      for (int32_t j = 0; j < P.min_inst && !err; ++j) { if (live + 1 > P.I) err = true; else live += 1; }
-    }
-  }
-  if (err) v.h[H_ERR] = 6;
-}
-
-// B3b (leader, control arm): the deferred enqueues of b3a's boundary, in the paper's order.
-static __device__ void b3b(Scn& c, int32_t total) {
-  DILU_VIEW(v, c);
-  const Params& P = *c.P;
-  for (int32_t e = 0; e < total; ++e) {
-    const int32_t f = v.fList[e];
-    if (v.fFlag[f] & EV_OUT)
-      for (int32_t j = 0; j < v.fK[f]; ++j) enqueue(c, f, 1);
-  }
-  for (int32_t e = 0; e < total; ++e) {
-    const int32_t f = v.fList[e];
-    if (!(v.fFlag[f] & EV_ARR)) continue;
-    if (v.fKind[f] == K_TRAIN) enqueue(c, f, v.fNw[f]);
-    else for (int32_t j = 0; j < P.min_inst; ++j) enqueue(c, f, 1);
-  }
-}
-
 // Returns whether a placement pass is due.  ovl (overlapped slots): the pass is left to
 // the caller, which runs it in warp 0 beside P0/P1/P2.
 static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, bool ovl = false) {
@@ -1863,7 +1804,7 @@ static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
     for (int32_t e = 0; e < total; ++e) {     // step 2: departures
       const int32_t f = v.fList[e];
       if (!(v.fFlag[f] & EV_DEP)) continue;
-      kill_queue_entries_of(v, f);
+      kill_queue_entries_of(c, f);
       while (v.fLh[f] >= 0) terminate(c, v.fLh[f]);
       v.fReg[f] = 0;
     }
@@ -1886,7 +1827,7 @@ static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
     for (int32_t e = 0; e < total && !v.h[H_ERR]; ++e) {     // step 4: arrivals
       const int32_t f = v.fList[e];
       if (!(v.fFlag[f] & EV_ARR)) continue;
-      register_func(v, f, t, P.Tp);
+      register_func(c, f, t, P.Tp);
       if (v.fKind[f] == K_TRAIN) enqueue(c, f, v.fNw[f]);
       else for (int32_t j = 0; j < P.min_inst && !v.h[H_ERR]; ++j) enqueue(c, f, 1);
     }
@@ -1980,7 +1921,7 @@ static __device__ void run_scenario(const Params& P, Red& red, View* sv, uint8_t
       for (int32_t j = 0; j < n_req && !v.h[H_ERR]; ++j) {
         if (req_scn[j] != sc) continue;
         const int32_t f = req_func[j];
-        register_func(v, f, t0, P.Tp);
+        register_func(c, f, t0, P.Tp);
         out_iid[j] = enqueue(c, f, v.fKind[f] == K_TRAIN ? v.fNw[f] : 1);
       }
     }
@@ -2014,98 +1955,6 @@ static __device__ void run_scenario(const Params& P, Red& red, View* sv, uint8_t
       // host's P.ovl): what the pass commits is cold in this slot, so P0/P1/P2 never count
       // it; pending instances read as not ready (iReady = BIG), rows only grow past gNs.
       const bool ovl = !fused && !alg2 && !lat && P.ovl;
-      if (ovl && P.ovl == 2) {
-        // Pipelined slot.  Serial part: warp 0 compacts the boundary's event
-        // flags (written by the previous slot's B1 shares), the leader applies B3a, one
-        // barrier, repack if residency changed.  Then two arms: warp 0 = control (B3b
-        // enqueues, the placement pass, the active-set fold, its B1 share of the next
-        // boundary once P0 has folded this slot's arrivals into fAcc), warps 1.. = P0 ->
-        // their B1 shares -> P1 -> P2 on the state after B3a.  One join barrier.
-        const bool bnd = P.SPS == 1 || t % P.SPS == 0;
-        TICK(0);
-        if (bnd && t == t0) {                            // prologue: this call's first B1
-          b1_share<0>(c, t);
-          __syncthreads();
-        }
-        int32_t total = 0;
-        if (bnd) {
-          if (threadIdx.x < 32) {
-            total = compact_events(c);
-            if (total > 0 && c.g.leader()) b3a(c, t, total, acc);
-            if (threadIdx.x == 0) v.h[H_PNEV] = total;
-          }
-          __syncthreads();
-          total = v.h[H_PNEV];
-          if (v.h[H_ERR]) break;                         // uniform after the barrier
-        }
-        const bool pass = bnd && (total > 0 || v.h[H_QLEN] > 0);
-        TICK(1);
-        if (v.h[H_DIRTY]) {
-          rebuild_layout(c);
-          if (c.g.leader()) acc.z->st[S_LAYOUT] += 1;
-        }
-        TICK(2);
-        const int32_t tn = t + 1;
-        const bool next_b1 = tn < t0 + n_slots && (P.SPS == 1 || tn % P.SPS == 0);
-        if (threadIdx.x < 32) {
-          if (total > 0 && c.g.leader()) b3b(c, total);
-          __syncwarp();
-          if (next_b1)                       // B3b's live counts are final for the B1 shares
-            asm volatile("bar.arrive 3, %0;" :: "r"((int)blockDim.x) : "memory");
-          if (pass) placement_pass<true>(c, red, ph, t, acc);
-          if (c.g.leader()) {        // after the pass: this slot's active set
-            const long long na = v.h[H_NACT];
-            acc.z->act += na;
-            acc.z->memu += na * P.M - v.h[H_SUMU];
-            acc.z->rows += P.G;
-            acc.z->maxa = na > acc.z->maxa ? na : acc.z->maxa;
-            acc.z->st[S_SLOT] += 1;
-          }
-          TICK(3);
-          if (next_b1) {
-            asm volatile("bar.sync 2, %0;" :: "r"((int)blockDim.x) : "memory");   // P0(t) done
-            b1_share<0>(c, tn);
-          }
-          TICK(4);
-        } else {
-          Scn cw = c;
-          cw.g.off = 32;
-          const int nb = (int)blockDim.x - 32;
-#ifdef DILU_PHASE_TIMING
-          long long w0 = clock64(), w1;   // worker arm, first worker thread: st[19..21]
-          const long long w_arm0 = w0;
-#define WTICK(k) do { w1 = clock64(); if (threadIdx.x == 32) acc.z->st[k] += w1 - w0; w0 = w1; } while (0)
-#else
-#define WTICK(k) do { } while (0)
-#endif
-          phase0<false>(cw, t, acc);
-          asm volatile("bar.sync 1, %0;" :: "r"(nb) : "memory");   // every P0(t) fold done
-          WTICK(19);
-          if (next_b1) {
-            asm volatile("bar.arrive 2, %0;" :: "r"((int)blockDim.x) : "memory");   // for warp 0's share
-            asm volatile("bar.sync 3, %0;" :: "r"((int)blockDim.x) : "memory");     // B3b done
-            b1_share<1>(c, tn);              // c: the thread's fixed B1 range
-          }
-          phase1<false>(cw, t, acc);
-          asm volatile("bar.sync 1, %0;" :: "r"(nb) : "memory");
-          WTICK(20);
-          phase2<false>(cw, t, acc);
-          WTICK(21);
-#ifdef DILU_PHASE_TIMING
-          {   // st[23]: per slot, the slowest worker's finish (since the arm start) via shared max
-            const long long mine = clock64() - w_arm0;
-            atomicMax(reinterpret_cast<unsigned long long*>(&acc.z->st[22]), (unsigned long long)mine);
-          }
-#endif
-#undef WTICK
-        }
-        __syncthreads();     // join
-#ifdef DILU_PHASE_TIMING
-        if (c.g.leader()) { acc.z->st[23] += acc.z->st[22]; acc.z->st[22] = 0; }
-#endif
-        TICK(5);
-        continue;
-      }
       if (ovl) {
         bool pass = false;
         TICK(0);

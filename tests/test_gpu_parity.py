@@ -95,16 +95,13 @@ def test_c4_sample_full_hour():
 
 
 @pytest.mark.parametrize("mode", ["cta_threads64", "cta_threads1024", "cta_no_smem", "cta_no_ovl",
-                                  "cta_pipe", "cta_pipe_threads96", "cluster_k1", "cluster_k3"])
+                                  "cta_threads96", "cluster_k1", "cluster_k3"])
 def test_launch_shape_invariance(mode, monkeypatch):
     """Both engines and several launch shapes give bit-identical results (45 scenarios)."""
     full = di.c4(n_scenarios=4096, T=600)
     wl = full.subset(np.arange(5, 4096, 91))
     engine, _, shape = mode.partition("_")
     monkeypatch.setenv("DILU_ENGINE", engine)
-    if shape.startswith("pipe"):     # pipelined overlapped slot (DILU_PIPE, DESIGN.md s5)
-        monkeypatch.setenv("DILU_PIPE", "1")
-        shape = shape[5:]
     if shape == "threads96":
         monkeypatch.setenv("DILU_THREADS", "96")
     if shape == "threads64":
