@@ -24,7 +24,8 @@ using namespace dilu;
 struct dilu_sim {
   dilu_config cfg;
   int engine;          // 0: CTA per scenario, 2: cluster per scenario
-  int K;               // cluster engine: CTAs per scenario
+  int K;               // cluster engine: CTAs per scenario group
+  int Kc;              // cluster engine: CTAs per hardware cluster (K = m * Kc)
   Layout L;
   Params P;
   cudaStream_t stream;
@@ -229,7 +230,7 @@ dilu_status launch_run(dilu_sim* s, int32_t n_slots, int32_t n_req, const int32_
     lc.stream = s->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = s->K;
+    at[0].val.clusterDim.x = s->Kc;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
@@ -333,6 +334,7 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   P.max_stages = cfg->max_llm_stages; P.flags = cfg->flags; P.Tp = cfg->pattern_len;
   P.T_slot = 1000LL * cfg->slot_ms;
   P.ovl = 0;
+  P.gK = 1;
 
   s->engine = choose_engine(cfg);
   int dev = 0;
@@ -346,20 +348,24 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
       return rc;
     int n_sm = 0;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    int want = n_sm / (cfg->n_scenarios > 0 ? cfg->n_scenarios : 1);
-    if (const char* e = getenv("DILU_CLUSTER")) want = atoi(e);
-    // Largest cluster size that keeps every scenario resident in one wave (a cluster of
-    // 16 must fit inside one GPC, so 148 SMs do not always hold 148/16 of them); when no
-    // size does, the one with the fewest waves.
+    // Scenario groups of K = m x Kc CTAs (m hardware clusters of Kc): the largest K that
+    // keeps every scenario's group resident in one wave (the groups spin on scenario-wide
+    // barriers), preferring larger clusters at equal K (the placement pass runs in the
+    // leader's cluster with hardware cluster barriers).  DILU_CLUSTER (Kc) / DILU_GROUP (K)
+    // are tuning / test hooks; results never depend on the shape.
     const int S = cfg->n_scenarios > 0 ? cfg->n_scenarios : 1;
-    int K = 0, best_waves = 0;
-    for (int k = want >= 16 ? 16 : (want < 1 ? 1 : want); k >= 1; --k) {   // any size 1..16
+    int want_kc = 0, want_k = 0;
+    if (const char* e = getenv("DILU_CLUSTER")) want_kc = atoi(e);
+    if (const char* e = getenv("DILU_GROUP")) want_k = atoi(e);
+    int K = 0, Kc = 0, best_waves = 0;
+    for (int kc = 16; kc >= 1; --kc) {
+      if (want_kc > 0 && kc != want_kc) continue;
       cudaLaunchConfig_t lc = {};
-      lc.gridDim = dim3(k);
+      lc.gridDim = dim3(kc);
       lc.blockDim = dim3(s->threads);
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = k; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      at[0].val.clusterDim.x = kc; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
       lc.attrs = at;
       lc.numAttrs = 1;
       int nclusters = 0;
@@ -367,14 +373,29 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
         cudaGetLastError();
         continue;
       }
-      const int waves = (S + nclusters - 1) / nclusters;
-      if (K == 0 || waves < best_waves) { K = k; best_waves = waves; }
-      if (waves == 1) break;
+      int m = nclusters / S;                     // clusters per scenario, all resident
+      if (m * kc > KMAX) m = KMAX / kc;
+      if (want_k > 0) m = want_k / kc;
+      int waves = 1;
+      if (m < 1) {                                // more scenarios than resident clusters:
+        m = 1;                                    // one cluster each, in waves
+        waves = (S + nclusters - 1) / nclusters;
+      }
+      const int k = m * kc;
+      if (want_k > 0 && k != want_k) continue;
+      const bool better = K == 0 || waves < best_waves ||
+                          (waves == best_waves && (k > K * 21 / 20 || (k * 21 / 20 >= K && kc > Kc)));
+      if (better) { K = k; Kc = kc; best_waves = waves; }
     }
     if (K < 1) return fail(s, DILU_E_CUDA, "no schedulable cluster size");
+    if (K > Kc && best_waves > 1) { K = Kc; }     // multi-cluster groups need one wave
     s->K = K;
+    s->Kc = Kc;
+    s->P.gK = K;
+    P.gK = K;
     s->grid = cfg->n_scenarios * K;
-    if (getenv("DILU_VERBOSE")) fprintf(stderr, "dilu: cluster engine K=%d waves=%d\n", K, best_waves);
+    if (getenv("DILU_VERBOSE"))
+      fprintf(stderr, "dilu: cluster engine group K=%d (clusters of %d) waves=%d\n", K, Kc, best_waves);
     return dilu_sim_reset(s);
   }
   // CTA engine launch shape: one CTA per scenario; hot state in shared memory when it fits
@@ -475,6 +496,15 @@ dilu_status dilu_sim_reset(dilu_sim* s) {
   s->t = 0;
   dilu_status rc = cuda_check(s, cudaMemsetAsync(s->P.state, 0, (size_t)s->cfg.n_scenarios * s->L.bytes, s->stream),
                               "state reset");
+  if (rc) return rc;
+  // the RPS rings too: the next-second evictee is prefetched before a window is full
+  // (its value is only used once W samples exist) -- defined bytes for initcheck
+  rc = cuda_check(s, cudaMemsetAsync(s->P.ring, 0, (size_t)s->cfg.n_scenarios * s->cfg.max_funcs * s->cfg.window_s * 4,
+                                     s->stream), "ring reset");
+  if (rc) return rc;
+  // group scratch: the multi-cluster barrier counters start at zero
+  rc = cuda_check(s, cudaMemsetAsync(s->P.gscratch, 0, (size_t)s->cfg.n_scenarios * GSCR * 8, s->stream),
+                  "scratch reset");
   if (rc) return rc;
   if (s->L.N) k_init<true><<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P);
   else k_init<false><<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P);

@@ -47,10 +47,12 @@ struct Params {
   int32_t S, G, F, I, W, M, Q, aw, bw, slot_ms, SPS, phi_out, phi_in, min_inst, max_stages,
       flags, Tp;
   int32_t ovl;               // overlapped slots: CTA engine, VAR 0, G <= 256, cold >= 1
+  int32_t gK;                // cluster engine: CTAs per scenario group (a multiple of the cluster size)
   int64_t T_slot;
 };
 
-constexpr int GSCR = 96;     // u64 words of per-scenario cluster scratch
+constexpr int KMAX = 160;    // CTAs per scenario group (multi-cluster groups)
+constexpr int GSCR = 4 * KMAX + 48;   // u64 words of per-scenario group scratch
 
 struct Acc0 {  // thread-0 tallies, kept in shared memory (not in every thread's registers)
   long long act, memu, rows, pok, pfail, cold, sout, sin, split, maxa;
@@ -157,11 +159,39 @@ static __device__ __forceinline__ void cluster_sync_all() {
                ::: "memory");
 }
 
+// Scenario-wide barrier across several clusters (multi-cluster groups): one
+// arrival per CTA on a per-scenario counter in global memory, the last arrival advances
+// the generation; every thread then fences (acquire at GPU scope) so it observes the other
+// CTAs' state writes -- the pattern of a cooperative grid sync, restricted to the scenario.
+static __device__ __forceinline__ void group_barrier(unsigned int* cnt, unsigned int* gen, int K) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int g;
+    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+    __threadfence();
+    if (atomicAdd(cnt, 1u) == (unsigned)K - 1) {
+      *cnt = 0;
+      __threadfence();
+      asm volatile("st.release.gpu.u32 [%0], %1;" :: "l"(gen), "r"(g + 1) : "memory");
+    } else {
+      unsigned int x;
+      do {
+        __nanosleep(64);
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(x) : "l"(gen) : "memory");
+      } while (x == g);
+    }
+  }
+  __syncthreads();
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
 struct Grp {
   int K, crank, cph;
+  int Kc;                    // CTAs per hardware cluster (K = m * Kc clusters of the scenario)
   int off;                   // threads [0, off) sit out (overlapped slots: warp 0 places)
-  unsigned long long* gu;    // [2][16] cluster scratch (u64)
-  int32_t* gi;               // [2][16] cluster scratch (i32)
+  unsigned long long* gu;    // [2][KMAX] group scratch (u64)
+  int32_t* gi;               // [2][KMAX] group scratch (i32)
+  unsigned int* bar;         // [2] multi-cluster barrier: arrivals, generation
   __device__ int rank() const { return crank * blockDim.x + threadIdx.x - off; }
   __device__ int size() const { return K * blockDim.x - off; }
   __device__ int wrank() const { return (crank * blockDim.x + threadIdx.x - off) >> 5; }
@@ -169,8 +199,12 @@ struct Grp {
   __device__ bool leader() const { return crank == 0 && threadIdx.x == 0; }
   __device__ bool lead_warp() const { return crank == 0 && threadIdx.x < 32; }
   __device__ void sync() const {
-    if (K == 1) __syncthreads(); else cluster_sync_all();
+    if (K == 1) __syncthreads();
+    else if (K == Kc) cluster_sync_all();
+    else group_barrier(bar, bar + 1, K);
   }
+  // the leader's hardware cluster alone (the placement pass of multi-cluster groups)
+  __device__ Grp first_cluster() const { Grp g = *this; g.K = Kc; return g; }
 };
 
 // ------------------------------------------------------------------ scenario
@@ -217,7 +251,7 @@ static __device__ __forceinline__ bool is_inf(int32_t k) { return k == K_INF || 
 static __device__ unsigned long long g_min_u64(Scn& c, unsigned long long v, Red& red, int& ph) {
   v = block_min_u64(v, red, ph);
   if (c.g.K == 1) return v;
-  unsigned long long* buf = c.g.gu + (c.g.cph & 1) * 16;
+  unsigned long long* buf = c.g.gu + (c.g.cph & 1) * KMAX;
   if (threadIdx.x == 0) buf[c.g.crank] = v;
   c.g.cph ^= 1;
   cluster_sync_all();
@@ -227,7 +261,7 @@ static __device__ unsigned long long g_min_u64(Scn& c, unsigned long long v, Red
 }
 static __device__ int32_t g_sum_i32(Scn& c, int32_t cta_value) {   // cta_value uniform within the CTA
   if (c.g.K == 1) return cta_value;
-  int32_t* buf = c.g.gi + (c.g.cph & 1) * 16;
+  int32_t* buf = c.g.gi + (c.g.cph & 1) * KMAX;
   if (threadIdx.x == 0) buf[c.g.crank] = cta_value;
   c.g.cph ^= 1;
   cluster_sync_all();
@@ -241,7 +275,7 @@ static __device__ int32_t g_scan(Scn& c, int32_t v, Red& red, int& ph, int32_t* 
   int32_t ctot;
   const int32_t pre = block_scan_i32(v, red, ph, &ctot);
   if (c.g.K == 1) { *total = ctot; return pre; }
-  int32_t* buf = c.g.gi + (c.g.cph & 1) * 16;
+  int32_t* buf = c.g.gi + (c.g.cph & 1) * KMAX;
   if (threadIdx.x == 0) buf[c.g.crank] = ctot;
   c.g.cph ^= 1;
   cluster_sync_all();
@@ -847,10 +881,19 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
 
 // The placement pass by the cheapest group: warp 0 alone for CTA-engine scenarios with
 // few GPUs (then one CTA barrier publishes its commits), else the whole group.
+// Multi-cluster groups place within the leader's hardware cluster alone (fast cluster
+// barriers per attempt); the other clusters wait at one scenario-wide barrier.
 static __device__ void placement(Scn& c, Red& red, int& ph, int32_t t, Acc& acc) {
   if (c.g.K == 1 && c.P->G <= WARP_PLACE_MAX) {
     if (threadIdx.x < 32) placement_pass<true>(c, red, ph, t, acc);
     __syncthreads();
+  } else if (c.g.K > c.g.Kc) {
+    if (c.g.crank < c.g.Kc) {
+      Scn cp = c;
+      cp.g = c.g.first_cluster();
+      placement_pass<false>(cp, red, ph, t, acc);
+    }
+    c.g.sync();
   } else {
     placement_pass<false>(c, red, ph, t, acc);
   }
@@ -1855,7 +1898,7 @@ template <bool SMEM, int VAR>
 static __device__ void run_scenario(const Params& P, Red& red, View* sv, uint8_t* smem, int32_t sc, int32_t t0,
                              int32_t n_slots, int32_t n_req, const int32_t* req_scn,
                              const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid,
-                             int K = 1, int crank = 0) {
+                             int K = 1, int crank = 0, int Kc = 1) {
   uint8_t* gblock = P.state + (size_t)sc * P.L.bytes;
   uint8_t* hot = gblock;
   if (SMEM) {
@@ -1884,15 +1927,17 @@ static __device__ void run_scenario(const Params& P, Red& red, View* sv, uint8_t
   c.g.crank = crank;
   c.g.cph = 0;
   c.g.off = 0;
+  c.g.Kc = Kc;
   c.g.gu = P.gscratch + (size_t)sc * GSCR;
-  c.g.gi = reinterpret_cast<int32_t*>(c.g.gu + 32);
-  int32_t* const mem = K == 1 ? red.members : reinterpret_cast<int32_t*>(c.g.gu + 48);
+  c.g.gi = reinterpret_cast<int32_t*>(c.g.gu + 2 * KMAX);
+  c.g.bar = reinterpret_cast<unsigned int*>(c.g.gu + 3 * KMAX);
+  int32_t* const mem = K == 1 ? red.members : reinterpret_cast<int32_t*>(c.g.gu + 3 * KMAX + 8);
 #ifdef DILU_BOUNDS
   c.members = Chk<int32_t>(mem, 64, DILU_ID_MEMBERS);
 #else
   c.members = mem;
 #endif
-  c.flag = K == 1 ? red.flag : reinterpret_cast<int32_t*>(c.g.gu + 80);
+  c.flag = K == 1 ? red.flag : reinterpret_cast<int32_t*>(c.g.gu + 3 * KMAX + 40);
   c.frow = P.funcs + (size_t)sc * P.F * 16;
   {
     const int32_t per = (P.F + c.g.size() - 1) / c.g.size();
@@ -2178,13 +2223,14 @@ k_run_cluster(const __grid_constant__ Params Pin, int32_t t0, int32_t n_slots, i
               const int32_t* req_func, int32_t* out_gpu, int32_t* out_iid) {
   __shared__ Red red;
   __shared__ View sv;
-  unsigned int crank, csize;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  unsigned int csize;
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
-  const int32_t sc = blockIdx.x / csize;
-  if (sc >= Pin.S) return;   // whole clusters only: uniform across the cluster
+  // a scenario's group: Pin.gK consecutive CTAs = Pin.gK / csize whole hardware clusters
+  const int32_t K = Pin.gK;
+  const int32_t sc = blockIdx.x / K;
+  if (sc >= Pin.S) return;   // whole groups only: uniform across the group
   run_scenario<false, VAR>(Pin, red, &sv, nullptr, sc, t0, n_slots, n_req, req_scn, req_func, out_gpu,
-                      out_iid, (int)csize, (int)crank);
+                      out_iid, (int)K, (int)(blockIdx.x % K), (int)csize);
 }
 
 #ifndef DILU_VARIANT_TU   // the init / snapshot kernels live in dilu_api.cu's unit only

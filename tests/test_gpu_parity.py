@@ -492,3 +492,17 @@ def test_modes_directional_c4_slice():
     act = {m: tot[m][T["gpu_slots_active"]] for m in tot}
     assert act[0] <= act[2] and act[0] <= act[1], act
     assert tot[0][T["cold_starts"]] <= tot[4][T["cold_starts"]]
+
+
+@pytest.mark.parametrize("shape", ["g8c2", "g6c3", "g4c1"])
+def test_multicluster_groups(shape, monkeypatch):
+    """Scenario groups of several hardware clusters (scenario-wide barriers in global
+    memory, placement inside the leader's cluster): C2, a C5-shaped reduced
+    trace and fused 100 ms batches, bit-exact against the oracle."""
+    k, kc = shape[1:].split("c")
+    monkeypatch.setenv("DILU_ENGINE", "cluster")
+    monkeypatch.setenv("DILU_GROUP", k)
+    monkeypatch.setenv("DILU_CLUSTER", kc)
+    run_pair(di.c2(seed=7, T=600), [1, 299, 300], id_cap=4096)
+    wl = di.scaled("C5g", 2048, 200, 400, 1200, 100, 900, [52, 53], max_instances=8192)
+    run_pair(wl, [1, 13, 886], id_cap=8192, snap=False)
