@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--prof-sessions", type=int, default=4096 * 200)
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"])
     ap.add_argument("--slots", type=int, default=0, help="slots per step (0: workload default)")
+    ap.add_argument("--scenarios", type=int, default=0,
+                    help="C5: scenarios in the batch (0: the 8 of BASELINE's C5; 1 = one 8-GPU strong shard)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample scenarios (0: auto)")
     ap.add_argument("--cpu-slots", type=int, default=0, help="oracle sample slots (0: the step's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -110,9 +112,9 @@ def world_env():
 # ------------------------------------------------------------------ workloads
 
 def build_workload(name: str, rank: int, world: int, scaling: str, slots: int,
-                   vertical: str = "slot", latency: bool = False):
+                   vertical: str = "slot", latency: bool = False, n_c5: int = 0):
     import dilu_inputs as di
-    wl, desc, n = _build_workload(name, rank, world, scaling, slots)
+    wl, desc, n = _build_workload(name, rank, world, scaling, slots, n_c5)
     extra = (4 if vertical == "alg2" else 0) | (8 if latency else 0)
     if extra:
         cfg = dict(wl.cfg, flags=wl.cfg["flags"] | extra)
@@ -124,7 +126,7 @@ def build_workload(name: str, rank: int, world: int, scaling: str, slots: int,
     return wl, desc, n
 
 
-def _build_workload(name: str, rank: int, world: int, scaling: str, slots: int):
+def _build_workload(name: str, rank: int, world: int, scaling: str, slots: int, n_c5: int = 0):
     import dilu_inputs as di
     if name == "C4":
         if scaling == "weak":
@@ -143,10 +145,11 @@ def _build_workload(name: str, rank: int, world: int, scaling: str, slots: int):
         return wl, "C3: one 1,024-GPU cluster, ~4,500 functions, diurnal (replica per rank)", slots or 3600
     if name == "C5":
         T = slots or 36000
+        tot = n_c5 or 8
         if scaling == "weak":
-            n, first = 8, 50 + 8 * rank
+            n, first = tot, 50 + tot * rank
         else:
-            lo, hi = 8 * rank // world, 8 * (rank + 1) // world
+            lo, hi = tot * rank // world, tot * (rank + 1) // world
             n, first = max(1, hi - lo), 50 + lo
         wl = di.c5(n_scenarios=n, T=T, first_seed=first)
         return wl, "C5: %d x 16,384-GPU clusters (seeds %d..%d), 100 ms slots, timed window" % (
@@ -305,7 +308,7 @@ def run_reference(args):
     if rank != 0:
         return
     wl, desc, n_slots = build_workload(args.workload, 0, 1, args.scaling, args.slots, args.vertical,
-                                       args.latency)
+                                       args.latency, args.scenarios)
     sub, slots, threads = oracle_sample(args, wl, n_slots)
     vals = []
     for k in range(args.warmup + args.steps):
@@ -357,7 +360,7 @@ def run_dilu(args):
     from paper_2503_05130_b200 import DiluSim, dist as ddist
     ddist.init("nccl", device=dev)
     wl, desc, n_slots = build_workload(args.workload, rank, world, args.scaling, args.slots,
-                                       args.vertical, args.latency)
+                                       args.vertical, args.latency, args.scenarios)
     sim = DiluSim.from_workload(wl, device=dev)
     stream = sim.stream
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)

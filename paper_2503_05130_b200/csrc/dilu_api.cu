@@ -383,8 +383,9 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
       }
       const int k = m * kc;
       if (want_k > 0 && k != want_k) continue;
+      // fewest waves, then the most CTAs per scenario, then the largest cluster
       const bool better = K == 0 || waves < best_waves ||
-                          (waves == best_waves && (k > K * 21 / 20 || (k * 21 / 20 >= K && kc > Kc)));
+                          (waves == best_waves && (k > K || (k == K && kc > Kc)));
       if (better) { K = k; Kc = kc; best_waves = waves; }
     }
     if (K < 1) return fail(s, DILU_E_CUDA, "no schedulable cluster size");

@@ -163,7 +163,7 @@ static __device__ __forceinline__ void cluster_sync_all() {
 // arrival per CTA on a per-scenario counter in global memory, the last arrival advances
 // the generation; every thread then fences (acquire at GPU scope) so it observes the other
 // CTAs' state writes -- the pattern of a cooperative grid sync, restricted to the scenario.
-static __device__ __forceinline__ void group_barrier(unsigned int* cnt, unsigned int* gen, int K) {
+static __device__ __noinline__ void group_barrier(unsigned int* cnt, unsigned int* gen, int K) {
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned int g;
@@ -199,9 +199,13 @@ struct Grp {
   __device__ bool leader() const { return crank == 0 && threadIdx.x == 0; }
   __device__ bool lead_warp() const { return crank == 0 && threadIdx.x < 32; }
   __device__ void sync() const {
+#if DILU_HOT_SMEM            // the shared-memory kernels run one CTA per scenario
+    __syncthreads();
+#else
     if (K == 1) __syncthreads();
     else if (K == Kc) cluster_sync_all();
     else group_barrier(bar, bar + 1, K);
+#endif
   }
   // the leader's hardware cluster alone (the placement pass of multi-cluster groups)
   __device__ Grp first_cluster() const { Grp g = *this; g.K = Kc; return g; }
@@ -254,7 +258,7 @@ static __device__ unsigned long long g_min_u64(Scn& c, unsigned long long v, Red
   unsigned long long* buf = c.g.gu + (c.g.cph & 1) * KMAX;
   if (threadIdx.x == 0) buf[c.g.crank] = v;
   c.g.cph ^= 1;
-  cluster_sync_all();
+  c.g.sync();                    // cluster barrier, or the scenario-wide one
   unsigned long long m = ~0ull;
   for (int k = 0; k < c.g.K; ++k) { const unsigned long long x = __ldcg(buf + k); m = x < m ? x : m; }
   return m;
@@ -264,7 +268,7 @@ static __device__ int32_t g_sum_i32(Scn& c, int32_t cta_value) {   // cta_value 
   int32_t* buf = c.g.gi + (c.g.cph & 1) * KMAX;
   if (threadIdx.x == 0) buf[c.g.crank] = cta_value;
   c.g.cph ^= 1;
-  cluster_sync_all();
+  c.g.sync();                    // cluster barrier, or the scenario-wide one
   int32_t r = 0;
   for (int k = 0; k < c.g.K; ++k) r += __ldcg(buf + k);
   return r;
@@ -278,7 +282,7 @@ static __device__ int32_t g_scan(Scn& c, int32_t v, Red& red, int& ph, int32_t* 
   int32_t* buf = c.g.gi + (c.g.cph & 1) * KMAX;
   if (threadIdx.x == 0) buf[c.g.crank] = ctot;
   c.g.cph ^= 1;
-  cluster_sync_all();
+  c.g.sync();                    // cluster barrier, or the scenario-wide one
   int32_t before = 0, tot = 0;
   for (int k = 0; k < c.g.K; ++k) {
     const int32_t x = __ldcg(buf + k);
@@ -887,6 +891,7 @@ static __device__ void placement(Scn& c, Red& red, int& ph, int32_t t, Acc& acc)
   if (c.g.K == 1 && c.P->G <= WARP_PLACE_MAX) {
     if (threadIdx.x < 32) placement_pass<true>(c, red, ph, t, acc);
     __syncthreads();
+#if !DILU_HOT_SMEM
   } else if (c.g.K > c.g.Kc) {
     if (c.g.crank < c.g.Kc) {
       Scn cp = c;
@@ -894,6 +899,7 @@ static __device__ void placement(Scn& c, Red& red, int& ph, int32_t t, Acc& acc)
       placement_pass<false>(cp, red, ph, t, acc);
     }
     c.g.sync();
+#endif
   } else {
     placement_pass<false>(c, red, ph, t, acc);
   }
