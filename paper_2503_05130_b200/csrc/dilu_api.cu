@@ -373,9 +373,13 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
         cudaGetLastError();
         continue;
       }
-      int m = nclusters / S;                     // clusters per scenario, all resident
+      const int m_res = nclusters / S;           // clusters per scenario with every group resident
+      // groups beyond ~32 CTAs gained nothing on C5 (scenario-wide barriers cost more than
+      // the extra SMs save), so at most 32 unless DILU_GROUP asks; never more
+      // than fit at once -- the groups spin on their barriers
+      int m = m_res < 32 / kc ? m_res : (32 / kc > 0 ? 32 / kc : 1);
+      if (want_k > 0) m = want_k / kc < m_res ? want_k / kc : m_res;
       if (m * kc > KMAX) m = KMAX / kc;
-      if (want_k > 0) m = want_k / kc;
       int waves = 1;
       if (m < 1) {                                // more scenarios than resident clusters:
         m = 1;                                    // one cluster each, in waves

@@ -175,9 +175,11 @@ static __device__ __noinline__ void group_barrier(unsigned int* cnt, unsigned in
       asm volatile("st.release.gpu.u32 [%0], %1;" :: "l"(gen), "r"(g + 1) : "memory");
     } else {
       unsigned int x;
+      long long spins = 0;
       do {
         __nanosleep(64);
         asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(x) : "l"(gen) : "memory");
+        if (++spins > (1ll << 24)) __trap();   // a group not resident as a whole: fail, do not hang
       } while (x == g);
     }
   }
