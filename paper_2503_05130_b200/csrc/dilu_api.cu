@@ -428,8 +428,14 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
     static const int cand[5] = {256, 224, 192, 160, 128};
     static const double lat[5] = {454, 457, 478, 495, 511};
     double best = 0.0;
+    cudaFuncAttributes fa = {};
+    if ((rc = cuda_check(s, cudaFuncGetAttributes(&fa, run_fn(true, variant_of(cfg, s->L))), "kernel attributes")))
+      return rc;
+    // (the one-slot-per-second kernel is compiled for 128 threads x 5 CTAs per SM)
+    if (s->threads > fa.maxThreadsPerBlock) s->threads = fa.maxThreadsPerBlock & ~31;
     for (int k = 0; k < 5; ++k) {
       int per = 0;
+      if (cand[k] > fa.maxThreadsPerBlock) continue;
       if ((rc = cuda_check(s, cudaFuncSetAttribute(run_fn(true, variant_of(cfg, s->L)),
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)s->L.hot_bytes), "smem attribute")))

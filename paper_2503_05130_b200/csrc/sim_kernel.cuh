@@ -138,7 +138,7 @@ static __device__ __forceinline__ int32_t block_scan_i32(int32_t v, Red& r, int&
 }
 
 #ifdef DILU_BOUNDS
-constexpr int DILU_ID_MEMBERS = 80;   // index of "members" in DILU_ARRAY_NAMES
+constexpr int DILU_ID_MEMBERS = 81;   // index of "members" in DILU_ARRAY_NAMES
 static __device__ __noinline__ void dilu_oob(int id, long long j, long long n) {
   const char* names[] = {DILU_ARRAY_NAMES};
   printf("DILU_BOUNDS: %s[%lld] outside [0, %lld) (block %d thread %d)\n",
@@ -310,7 +310,7 @@ static __device__ __forceinline__ View hot_view(const View& s) {
   View v = s;
 #define DILU_A(p) __builtin_assume(__isShared(v.p))
   DILU_A(h); DILU_A(gR); DILU_A(gL); DILU_A(gU); DILU_A(gRel); DILU_A(rlG); DILU_A(rlE);
-  DILU_A(gN); DILU_A(gNs); DILU_A(gExcl); DILU_A(gRes); DILU_A(gGrow); DILU_A(gMask);
+  DILU_A(gN); DILU_A(gNs); DILU_A(gExcl); DILU_A(gRes); DILU_A(gGrow); DILU_A(gMask); DILU_A(gChk);
   DILU_A(iId); DILU_A(iReady); DILU_A(iR); DILU_A(iFunc); DILU_A(iNext); DILU_A(fstack); DILU_A(iMeta);
   DILU_A(fKind); DILU_A(fPrio); DILU_A(fNw); DILU_A(fReq); DILU_A(fLim); DILU_A(fCb); DILU_A(fIbs);
   DILU_A(fCls); DILU_A(fDtr); DILU_A(fPat); DILU_A(fScale); DILU_A(fCap1); DILU_A(fReg); DILU_A(fNsamp);
@@ -452,7 +452,7 @@ static __device__ DILU_SERIAL void release(Scn& c, int32_t s) {
 }
 
 // terminate a live instance (placed or pending); frees its slot
-#ifdef DILU_PHASE_TIMING
+#if defined(DILU_PHASE_TIMING) && DILU_PHASE_TIMING != 2
 #define TSTART long long _t0 = clock64()
 #define TSTOP(k) do { if (c.g.leader()) c.z->st[k] += clock64() - _t0; } while (0)
 #else
@@ -962,6 +962,17 @@ static __device__ void rebuild_layout(Scn& c) {
       v.gGrow[v.h[H_GBASE + k] + idx] = g;   // order inside a class is irrelevant
     }
   }
+  // one descriptor per warp chunk: its first row in gGrow, its row count, its width class
+  const int32_t nch = v.h[H_CBASE + 6];
+  #pragma unroll 1
+  for (int32_t ch = c.g.rank(); ch < nch; ch += c.g.size()) {
+    int k = 0;
+    #pragma unroll
+    for (int x = 1; x < 6; ++x) k += (ch >= v.h[H_CBASE + x]);
+    const int32_t per = 32 >> k, i0 = (ch - v.h[H_CBASE + k]) * per;
+    const int32_t nv = min(per, v.h[H_CCNT + k] - i0);
+    v.gChk[ch] = (v.h[H_GBASE + k] + i0) | (nv << 16) | (k << 24);
+  }
   c.g.sync();
 }
 
@@ -1070,14 +1081,15 @@ static __device__ void phase0(Scn& c, int32_t t, Acc& acc) {
     acc.nfun += 1;
     facc[f] += A;
     acc.rtot += A;
-    int32_t nw = 0;
+    int32_t nw = 0, s1 = -1;
     for (int32_t s = lh[f]; s >= 0; s = nxt[s])
-      nw += (st_of(meta[s]) == ST_PLACED && ready[s] <= t);
+      if (st_of(meta[s]) == ST_PLACED && ready[s] <= t) { s1 = nw == 0 ? s : s1; ++nw; }
     if (nw == 0) {
       acc.rvio += A;
       if (LAT) lat_unserved(c.lat, A);
       continue;
     }
+    if (nw == 1) { r[s1] = A; continue; }   // one warm instance (the common case): no second walk
     const int32_t q = A / nw, rem = A - q * nw;
     int32_t rank = 0;
     for (int32_t s = lh[f]; s >= 0; s = nxt[s]) {
@@ -1122,21 +1134,18 @@ static __device__ void phase1(Scn& c, int32_t t, Acc& acc) {
   const auto fdtr = v.fDtr;
   const auto fibs = v.fIbs;
   const auto fcb = v.fCb;
-  const auto cbase = v.h + H_CBASE;
-  const auto ccnt = v.h + H_CCNT;
-  const auto gbase = v.h + H_GBASE;
-  const int32_t nch = cbase[6];
+  const auto chk = v.gChk;
+  const int32_t nch = v.h[H_CBASE + 6];
   const int32_t T = (int32_t)P.T_slot, slot_ms = P.slot_ms;
   const uint64_t ht = sm64(sm64((uint32_t)c.scn_id) ^ (uint32_t)t);   // mix() prefix, per slot
   for (int32_t ch = wid; ch < nch; ch += nwarp) {
-    int k = 0;
-#pragma unroll
-    for (int x = 1; x < 6; ++x) k += (ch >= cbase[x]);
+    const int32_t cd = chk[ch];
+    const int k = cd >> 24;
     const int w = 1 << k;
-    const int32_t gi = (ch - cbase[k]) * (32 >> k) + (lane >> k);
+    const int32_t gi = lane >> k;
     int32_t g = -1, s = -1;
-    if (gi < ccnt[k]) {
-      g = grow[gbase[k] + gi];
+    if (gi < ((cd >> 16) & 255)) {
+      g = grow[(cd & 0xFFFF) + gi];
       const int j = lane & (w - 1);
       if (j < gn[g]) s = gres[(size_t)g * RES + j];
     }
@@ -1345,21 +1354,18 @@ static __device__ void phase1_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
   DILU_VIEW(v, c);
   const Params& P = *c.P;
   const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
-  const auto cbase = v.h + H_CBASE;
-  const auto ccnt = v.h + H_CCNT;
-  const auto gbase = v.h + H_GBASE;
-  const int32_t nch = cbase[6];
+  const auto chk = v.gChk;
+  const int32_t nch = v.h[H_CBASE + 6];
   const int32_t T = (int32_t)P.T_slot, slot_ms = P.slot_ms, I = P.I, F = P.F;
   const uint64_t hs = sm64((uint32_t)c.scn_id);
   for (int32_t ch = wid; ch < nch; ch += nwarp) {
-    int k = 0;
-#pragma unroll
-    for (int x = 1; x < 6; ++x) k += (ch >= cbase[x]);
+    const int32_t cd = v.gChk[ch];
+    const int k = cd >> 24;
     const int w = 1 << k;
-    const int32_t gi = (ch - cbase[k]) * (32 >> k) + (lane >> k);
+    const int32_t gi = lane >> k;
     int32_t g = -1, s = -1;
-    if (gi < ccnt[k]) {
-      g = v.gGrow[gbase[k] + gi];
+    if (gi < ((cd >> 16) & 255)) {
+      g = v.gGrow[(cd & 0xFFFF) + gi];
       const int j = lane & (w - 1);
       if (j < v.gN[g]) s = v.gRes[(size_t)g * RES + j];
     }
@@ -1526,23 +1532,20 @@ static __device__ void phase1_alg2(Scn& c, int32_t t, int32_t B, DPN(const int32
   const Params& P = *c.P;
   const int lane = threadIdx.x & 31, wid = c.g.wrank(), nwarp = c.g.nwarps();
   const unsigned FULL = 0xffffffffu;
-  const auto cbase = v.h + H_CBASE;
-  const auto ccnt = v.h + H_CCNT;
-  const auto gbase = v.h + H_GBASE;
-  const int32_t nch = cbase[6];
+  const auto chk = v.gChk;
+  const int32_t nch = v.h[H_CBASE + 6];
   const int32_t NP = P.slot_ms / A2_PERIOD_MS;
   const long long PT = (long long)A2_PERIOD_MS * 1000;          // period in us
   const uint64_t hs = sm64((uint32_t)c.scn_id);
   for (int32_t ch = wid; ch < nch; ch += nwarp) {
-    int k = 0;
-#pragma unroll
-    for (int x = 1; x < 6; ++x) k += (ch >= cbase[x]);
+    const int32_t cd = v.gChk[ch];
+    const int k = cd >> 24;
     const int w = 1 << k;
     const int j = lane & (w - 1);
-    const int32_t gi = (ch - cbase[k]) * (32 >> k) + (lane >> k);
+    const int32_t gi = lane >> k;
     int32_t g = -1, s = -1;
-    if (gi < ccnt[k]) {
-      g = v.gGrow[gbase[k] + gi];
+    if (gi < ((cd >> 16) & 255)) {
+      g = v.gGrow[(cd & 0xFFFF) + gi];
       if (j < v.gN[g]) s = v.gRes[(size_t)g * RES + j];
     }
     // batch-invariant resident fields and its stage's Alg.2 state
@@ -1806,6 +1809,39 @@ static __device__ int32_t b1_func(Scn& c, int32_t f, int32_t sec) {
   return ev;
 }
 
+// Overlapped slots: after its placement pass warp 0 recounts the windows
+// of the functions whose live count n B3 just changed (ScaleOut / ScaleIn), against the
+// new thresholds n*cap1 and (n-1)*cap1, so that B1 of the next boundary -- where the whole
+// CTA waits for its slowest thread -- finds fThrn == n and only updates incrementally.
+// Exact: the counts cover the valid samples (ring[0, ns) before the ring first fills),
+// nothing but B1 writes the ring, and n cannot change before that B1 (placement does not
+// change live counts).  Counting before the ring is full only starts the incremental
+// counts earlier; at the first decision (ns >= W) they equal a full recount.
+static __device__ void prerecount_warp(Scn& c) {
+  DILU_VIEW(v, c);
+  __syncwarp();
+  const int lane = threadIdx.x & 31;
+  const int32_t ne = v.h[H_NEV], W = c.P->W;
+  if (c.mode == M_EAGER) return;                   // (reactive: no window counts)
+  #pragma unroll 1
+  for (int32_t e = 0; e < ne; ++e) {
+    const int32_t f = v.fList[e];
+    if (!(v.fFlag[f] & (EV_OUT | EV_IN)) || !v.fReg[f]) continue;
+    const int32_t n = v.fNlive[f];
+    if (v.fThrn[f] == n) continue;
+    const int32_t ns = v.fNsamp[f], cnt = ns < W ? ns : W;
+    const long long cap1 = v.fCap1[f], cu = (long long)n * cap1, cd = (long long)(n - 1) * cap1;
+    const auto ring = v.ring + (size_t)f * W;
+    int32_t up = 0, dn = 0;
+    #pragma unroll 1
+    for (int32_t j = lane; j < cnt; j += 32) { const int32_t w = ring[j]; up += w > cu; dn += w < cd; }
+    up = __reduce_add_sync(0xffffffffu, up);
+    dn = __reduce_add_sync(0xffffffffu, dn);
+    if (lane == 0) { v.fUp[f] = up; v.fDown[f] = dn; v.fThrn[f] = n; }
+  }
+  __syncwarp();
+}
+
 // Returns whether a placement pass is due.  ovl (overlapped slots): the pass is left to
 // the caller, which runs it in warp 0 beside P0/P1/P2.
 static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, bool ovl = false) {
@@ -1817,6 +1853,9 @@ static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
   const int32_t lo = c.b1lo, hi = c.b1hi;   // this thread's contiguous function range
   const auto fflag = v.fFlag;
   int32_t cnt = 0;
+#if defined(DILU_PHASE_TIMING) && DILU_PHASE_TIMING == 2
+  const long long fa = clock64();
+#endif
 #if DILU_HOT_SMEM
   cp_async_wait_all();                              // this thread's fOld / fPv copies landed
 #endif
@@ -1826,18 +1865,29 @@ static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
 #endif
 #ifdef DILU_PHASE_TIMING
   const long long cb0 = clock64();   // st[22]: B1 count barrier -> end of compaction (leader)
+#if DILU_PHASE_TIMING == 2
+  if (c.g.leader()) acc.z->st[15] += cb0 - fa;
+#endif
 #endif
   const int32_t any = g_count(c, cnt);
+#if defined(DILU_PHASE_TIMING) && DILU_PHASE_TIMING == 2
+  const long long fc = clock64();
+  if (c.g.leader()) acc.z->st[16] += fc - cb0;
+#endif
   int32_t total = 0;
   if (any) {                                        // ordered compaction of the events
     int32_t pos = g_scan(c, cnt, red, ph, &total);
     for (int32_t f = lo; f < hi && cnt; ++f)
       if (fflag[f]) { v.fList[pos++] = f; --cnt; }
     c.g.sync();                                     // the event list is complete before B3
+#if defined(DILU_PHASE_TIMING) && DILU_PHASE_TIMING == 2
+    if (c.g.leader()) acc.z->st[17] += clock64() - fc;
+#endif
   }
-#ifdef DILU_PHASE_TIMING
+#if defined(DILU_PHASE_TIMING) && DILU_PHASE_TIMING != 2
   if (c.g.leader()) acc.z->st[22] += clock64() - cb0;
 #endif
+  if (c.g.leader()) v.h[H_NEV] = total;            // (overlapped slots: prerecount_warp)
   const int32_t need_pass = total > 0 || v.h[H_QLEN] > 0;   // uniform: QLEN only changes in B3/placement
 #ifdef DILU_PHASE_TIMING
   long long bt0 = clock64();
@@ -2023,6 +2073,7 @@ static __device__ void run_scenario(const Params& P, Red& red, View* sv, uint8_t
         TICK(2);
         if (threadIdx.x < 32) {
           if (pass) placement_pass<true>(c, red, ph, t, acc);
+          if (pass) prerecount_warp(c);
           if (c.g.leader()) {        // after the pass: this slot's active set
             const long long na = v.h[H_NACT];
             acc.z->act += na;
@@ -2203,8 +2254,11 @@ static __device__ void run_scenario(const Params& P, Red& red, View* sv, uint8_t
 #endif
 constexpr int SMEM_MAX_THREADS = DILU_SMEM_THREADS;   // shared-memory variant: <= this many threads, DILU_MINB CTAs/SM
 
+// The one-slot-per-second shared-memory kernel (C4's) runs 128 threads x 5 scenarios per
+// SM (what the hot state allows): 96 registers per thread instead of 80 (no spills).
 template <bool SMEM, int VAR>
-__global__ void __launch_bounds__(SMEM ? SMEM_MAX_THREADS : 1024, SMEM ? DILU_MINB : 1)
+__global__ void __launch_bounds__(SMEM ? (VAR == 0 ? 128 : SMEM_MAX_THREADS) : 1024,
+                                  SMEM ? (VAR == 0 ? 5 : DILU_MINB) : 1)
 k_run(const __grid_constant__ Params Pin, int32_t* next_scn, int32_t t0,
                                               int32_t n_slots, int32_t n_req,
                                               const int32_t* req_scn, const int32_t* req_func,

@@ -64,7 +64,7 @@ struct Layout {
   int32_t N;               // narrow element types (ET<true>): CTA engine, hot region in smem
   // byte offsets inside one block
   size_t hdr;
-  size_t gR, gL, gU, gN, gNs, gRes, gExcl, gGrow, gMask, gRel, rlG, rlE;
+  size_t gR, gL, gU, gN, gNs, gRes, gExcl, gGrow, gMask, gChk, gRel, rlG, rlE;
   size_t iId, iFunc, iMeta, iReady, iG, iSh0, iShare, iNext, iR, iBmin, fstack;
   size_t fKind, fPrio, fReq, fLim, fMem, fCb, fIbs, fNw, fCold, fCls, fDtr, fPat, fScale,
       fPhase, fCap1;
@@ -96,6 +96,7 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B 
   L.gRes = take(X * (size_t)G * RES);
   L.gExcl = take(S1 * (size_t)G); L.gGrow = take(X * (size_t)G);
   L.gMask = take(8 * (size_t)G);        // bit (affinity_class & 63) per resident class
+  L.gChk = take(4 * ((size_t)G + 8));   // P1 warp-chunk descriptors (first row | rows << 16 | class << 24)
   L.rlG = take(4 * RLOG); L.rlE = take(4 * RLOG);
   L.iId = take(4 * (size_t)I); L.iFunc = take(X * (size_t)I); L.iMeta = take(S1 * (size_t)I);
   L.iReady = take(4 * (size_t)I); L.iNext = take(X * (size_t)I); L.iR = take(4 * 2 * (size_t)I);
@@ -226,6 +227,7 @@ template <bool N> struct ViewT {
   HS gN, gNs, gExcl;
   HX gRes, gGrow;
   HP(unsigned long long) gMask;
+  HI gChk;
   HI iId, iReady, iR;
   HX iFunc, iNext, fstack;
   HS iMeta;
@@ -291,6 +293,7 @@ inline ViewT<N> make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
   PT(X, gRes, G * RES); PT(S1, gExcl, G); PT(X, gGrow, G); PT(int32_t, gRel, G);
   PT(int32_t, rlG, RLOG); PT(int32_t, rlE, RLOG);
   PT(unsigned long long, gMask, G);
+  PT(int32_t, gChk, G + 8);
   PT(int32_t, iId, I); PT(X, iFunc, I); PT(S1, iMeta, I); PT(int32_t, iReady, I);
   PT(int32_t, iSh0, I); PT(int32_t, iShare, I * MAXST); PT(X, iNext, I); PT(int32_t, iR, 2 * I);
   PT(int32_t, iBmin, 2 * I); PT(X, fstack, I);
@@ -324,7 +327,7 @@ inline ViewT<N> make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
 }
 
 #define DILU_ARRAY_NAMES                                                                     \
-  "h", "gR", "gL", "gU", "gN", "gNs", "gRes", "gExcl", "gGrow", "gRel", "rlG", "rlE", "gMask", \
+  "h", "gR", "gL", "gU", "gN", "gNs", "gRes", "gExcl", "gGrow", "gRel", "rlG", "rlE", "gMask", "gChk", \
   "iId", "iFunc", "iMeta", "iReady", "iSh0", "iShare", "iNext", "iR", "iBmin", "fstack", "iG",  \
   "fKind", "fPrio", "fReq", "fLim", "fMem", "fCb", "fIbs", "fNw", "fCold", "fCls", "fDtr",     \
   "fPat", "fScale", "fPhase", "fCap1", "fReg", "fNsamp", "fAcc", "fHead", "fUp", "fDown",      \
