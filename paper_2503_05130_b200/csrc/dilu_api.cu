@@ -334,6 +334,7 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   P.max_stages = cfg->max_llm_stages; P.flags = cfg->flags; P.Tp = cfg->pattern_len;
   P.T_slot = 1000LL * cfg->slot_ms;
   P.ovl = 0;
+  P.covl = 0;
   P.gK = 1;
 
   s->engine = choose_engine(cfg);
@@ -341,6 +342,10 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
   cudaGetDevice(&dev);
   if (s->engine == 2) {
     s->threads = 1024;
+    if (const char* e = getenv("DILU_CTHREADS")) {   // tuning hook: threads per cluster CTA
+      const int v = atoi(e);
+      if (v >= 128 && v <= 1024 && v % 32 == 0) s->threads = v;
+    }
     s->use_smem = false;
     if ((rc = cuda_check(s, cudaFuncSetAttribute(cluster_fn(variant_of(cfg, s->L)),
                                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
@@ -377,7 +382,9 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
       // groups beyond ~32 CTAs gained nothing on C5 (scenario-wide barriers cost more than
       // the extra SMs save), so at most 32 unless DILU_GROUP asks; never more
       // than fit at once -- the groups spin on their barriers
-      int m = m_res < 32 / kc ? m_res : (32 / kc > 0 ? 32 / kc : 1);
+      int cap = 32;                               // CTAs per scenario (tuning hook DILU_KCAP)
+      if (const char* e = getenv("DILU_KCAP")) cap = atoi(e) > 0 ? atoi(e) : cap;
+      int m = m_res < cap / kc ? m_res : (cap / kc > 0 ? cap / kc : 1);
       if (want_k > 0) m = want_k / kc < m_res ? want_k / kc : m_res;
       if (m * kc > KMAX) m = KMAX / kc;
       int waves = 1;
@@ -399,8 +406,20 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
     s->P.gK = K;
     P.gK = K;
     s->grid = cfg->n_scenarios * K;
+    // Overlapped batches: the leader's cluster places while the other CTAs
+    // run the batch.  Exact only if nothing placed at a boundary turns warm inside that
+    // batch, i.e. every cold start >= one batch of slots.
+    {
+      bool cold_ok = true;
+      const size_t nf = (size_t)cfg->n_scenarios * cfg->max_funcs;
+      for (size_t i = 0; i < nf && cold_ok; ++i)
+        if (h_funcs[i].kind != -1 && h_funcs[i].cold_slots < s->L.B) cold_ok = false;
+      const char* e = getenv("DILU_NO_OVL");
+      P.covl = cold_ok && variant_of(cfg, s->L) == 1 && K > Kc && s->L.B > 1 && !(e && atoi(e));
+    }
     if (getenv("DILU_VERBOSE"))
-      fprintf(stderr, "dilu: cluster engine group K=%d (clusters of %d) waves=%d\n", K, Kc, best_waves);
+      fprintf(stderr, "dilu: cluster engine group K=%d (clusters of %d) waves=%d covl=%d\n", K, Kc,
+              best_waves, P.covl);
     return dilu_sim_reset(s);
   }
   // CTA engine launch shape: one CTA per scenario; hot state in shared memory when it fits

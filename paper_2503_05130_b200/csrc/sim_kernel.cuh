@@ -47,6 +47,7 @@ struct Params {
   int32_t S, G, F, I, W, M, Q, aw, bw, slot_ms, SPS, phi_out, phi_in, min_inst, max_stages,
       flags, Tp;
   int32_t ovl;               // overlapped slots: CTA engine, VAR 0, G <= 256, cold >= 1
+  int32_t covl;              // overlapped batches: cluster engine, VAR 1, K > Kc, every cold start >= one batch
   int32_t gK;                // cluster engine: CTAs per scenario group (a multiple of the cluster size)
   int64_t T_slot;
 };
@@ -191,6 +192,7 @@ struct Grp {
   int K, crank, cph;
   int Kc;                    // CTAs per hardware cluster (K = m * Kc clusters of the scenario)
   int off;                   // threads [0, off) sit out (overlapped slots: warp 0 places)
+  int sub;                   // > 0: the group minus its first `sub` CTAs (overlapped batches)
   unsigned long long* gu;    // [2][KMAX] group scratch (u64)
   int32_t* gi;               // [2][KMAX] group scratch (i32)
   unsigned int* bar;         // [2] multi-cluster barrier: arrivals, generation
@@ -206,6 +208,7 @@ struct Grp {
 #else
     if (K == 1) __syncthreads();
     else if (K == Kc) cluster_sync_all();
+    else if (sub) group_barrier(bar + 2, bar + 3, K - sub);   // own counter: runs beside the leader cluster
     else group_barrier(bar, bar + 1, K);
 #endif
   }
@@ -398,7 +401,7 @@ static __device__ DILU_SERIAL void commit(Scn& c, int32_t s, int32_t g, int32_t 
   v.h[H_SUMU] += share;
   const auto res = v.gRes + (size_t)g * RES;
   int pos = v.gN[g];
-  if (!c.P->ovl) {            // keep (prio, id) order now ...
+  if (!(c.P->ovl | c.P->covl)) {   // keep (prio, id) order now ...
     const long long k = res_key(v, s);
     #pragma unroll 1
     while (pos > 0 && res_key(v, res[pos - 1]) > k) { res[pos] = res[pos - 1]; --pos; }
@@ -921,7 +924,7 @@ static __device__ void rebuild_layout(Scn& c) {
   #pragma unroll 1
   for (int32_t g = c.g.rank(); g < P.G; g += c.g.size()) {
     const int32_t n = v.gN[g];
-    if (P.ovl && n > 1) {     // overlapped slots append commits: restore (prio, id) order
+    if ((P.ovl | P.covl) && n > 1) {   // overlapped slots / batches append commits: restore (prio, id) order
       const auto res = v.gRes + (size_t)g * RES;
       long long kp = res_key(v, res[0]);
       #pragma unroll 1
@@ -1367,7 +1370,7 @@ static __device__ void phase1_b(Scn& c, int32_t t, int32_t B, Acc& acc) {
     if (gi < ((cd >> 16) & 255)) {
       g = v.gGrow[(cd & 0xFFFF) + gi];
       const int j = lane & (w - 1);
-      if (j < v.gN[g]) s = v.gRes[(size_t)g * RES + j];
+      if (j < (P.covl ? v.gNs[g] : v.gN[g])) s = v.gRes[(size_t)g * RES + j];   // gNs: see covl
     }
     // batch-invariant resident fields
     bool placed = false;
@@ -1933,7 +1936,7 @@ static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
       else for (int32_t j = 0; j < P.min_inst && !v.h[H_ERR]; ++j) enqueue(c, f, 1);
     }
   }
-  if (ovl && any) __syncthreads();   // B3's state changes before P0/P1/P2 and the repack
+  if (ovl && total > 0) c.g.sync();   // B3's state changes before P0/P1/P2 and the repack
 #ifdef DILU_PHASE_TIMING
   if (c.g.leader()) acc.z->st[14] += clock64();
 #endif
@@ -1985,6 +1988,7 @@ static __device__ void run_scenario(const Params& P, Red& red, View* sv, uint8_t
   c.g.crank = crank;
   c.g.cph = 0;
   c.g.off = 0;
+  c.g.sub = 0;
   c.g.Kc = Kc;
   c.g.gu = P.gscratch + (size_t)sc * GSCR;
   c.g.gi = reinterpret_cast<int32_t*>(c.g.gu + 2 * KMAX);
@@ -2117,6 +2121,60 @@ static __device__ void run_scenario(const Params& P, Red& red, View* sv, uint8_t
         TICK(5);
         continue;
       }
+#if !DILU_HOT_SMEM
+      if (fused && !alg2 && !lat && P.covl) {
+        // overlapped batch (cluster engine): the leader's hardware cluster runs
+        // the placement pass while the other CTAs of the group run P0b/P1b/P2b over the
+        // state after B3.  Exact when every cold start is at least one batch (the host's
+        // P.covl): what the pass commits is cold for the whole batch, so the batch never
+        // counts it; rows only grow past gNs (commits append, the next repack sorts).
+        bool pass = false;
+        TICK(0);
+        if (P.SPS == 1 || t % P.SPS == 0) {
+          pass = boundary(c, red, ph, t, acc, true);   // B1 + B3 (+ barrier)
+          if (v.h[H_ERR]) break;                       // uniform after B3's barrier
+        }
+        TICK(1);
+        if (v.h[H_DIRTY]) {
+          rebuild_layout(c);
+          if (c.g.leader()) acc.z->st[S_LAYOUT] += 1;
+        }
+        TICK(2);
+        int32_t B = P.SPS - t % P.SPS;
+        if (B > t0 + n_slots - t) B = t0 + n_slots - t;
+        if (B > P.L.B) B = P.L.B;
+        if (t % P.SPS != 0) c.g.sync();   // previous batch's P2 has read rB / bB
+        if (c.g.crank < c.g.Kc) {
+          if (pass) {
+            Scn cp = c;
+            cp.g = c.g.first_cluster();
+            placement_pass<false>(cp, red, ph, t, acc);
+          }
+          if (c.g.leader()) {        // after the pass: this batch's active set
+            const long long na = v.h[H_NACT];
+            acc.z->act += na * B;
+            acc.z->memu += (na * P.M - v.h[H_SUMU]) * B;
+            acc.z->rows += (long long)P.G * B;
+            acc.z->maxa = na > acc.z->maxa ? na : acc.z->maxa;
+            acc.z->st[S_SLOT] += B;
+          }
+          TICK(3);
+        } else {
+          Scn cw = c;
+          cw.g.off = c.g.Kc * (int)blockDim.x;
+          cw.g.sub = c.g.Kc;
+          phase0_b<false>(cw, t, B, acc);
+          cw.g.sync();
+          phase1_b<false>(cw, t, B, acc);
+          cw.g.sync();
+          phase2_b<false>(cw, t, B, acc);
+        }
+        c.g.sync();                  // join
+        TICK(5);
+        t += B - 1;
+        continue;
+      }
+#endif
       if (P.SPS == 1 || t % P.SPS == 0) {
         // no barrier here: B1 touches only the per-function window fields, which P2(t-1)
         // never reads, and B1's own count barrier orders P2(t-1) before B3 mutates state

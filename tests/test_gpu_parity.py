@@ -494,11 +494,16 @@ def test_modes_directional_c4_slice():
     assert tot[0][T["cold_starts"]] <= tot[4][T["cold_starts"]]
 
 
-@pytest.mark.parametrize("shape", ["g8c2", "g6c3", "g4c1"])
+@pytest.mark.parametrize("shape", ["g8c2", "g6c3", "g4c1", "g8c2serial"])
 def test_multicluster_groups(shape, monkeypatch):
     """Scenario groups of several hardware clusters (scenario-wide barriers in global
     memory, placement inside the leader's cluster): C2, a C5-shaped reduced
-    trace and fused 100 ms batches, bit-exact against the oracle."""
+    trace and fused 100 ms batches, bit-exact against the oracle -- with the placement pass
+    overlapped with the batch (the default when every cold start is >= one batch) and, for
+    `serial`, without."""
+    if shape.endswith("serial"):
+        monkeypatch.setenv("DILU_NO_OVL", "1")
+        shape = shape[:-len("serial")]
     k, kc = shape[1:].split("c")
     monkeypatch.setenv("DILU_ENGINE", "cluster")
     monkeypatch.setenv("DILU_GROUP", k)
