@@ -139,7 +139,7 @@ static __device__ __forceinline__ int32_t block_scan_i32(int32_t v, Red& r, int&
 }
 
 #ifdef DILU_BOUNDS
-constexpr int DILU_ID_MEMBERS = 81;   // index of "members" in DILU_ARRAY_NAMES
+constexpr int DILU_ID_MEMBERS = 82;   // index of "members" in DILU_ARRAY_NAMES
 static __device__ __noinline__ void dilu_oob(int id, long long j, long long n) {
   const char* names[] = {DILU_ARRAY_NAMES};
   printf("DILU_BOUNDS: %s[%lld] outside [0, %lld) (block %d thread %d)\n",
@@ -392,23 +392,40 @@ static __device__ __forceinline__ long long res_key(const View& v, int32_t s) {
 
 static __device__ DILU_SERIAL void commit(Scn& c, int32_t s, int32_t g, int32_t share) {
   DILU_VIEW(v, c);
+  // every value read before any write: the reads are independent, so they overlap (the
+  // rows are in HBM/L2 on the cluster engine, where each dependent read is a round trip)
   const int32_t f = v.iFunc[s];
-  if (v.gN[g] == 0) v.h[H_NACT] += 1;
-  v.gMask[g] |= 1ull << (v.fCls[f] & 63);
-  v.gR[g] += v.fReq[f];
-  v.gL[g] += v.fLim[f];
-  v.gU[g] += share;
-  v.h[H_SUMU] += share;
+  const int32_t n0 = v.gN[g], R0 = v.gR[g], L0 = v.gL[g], U0 = v.gU[g];
+  const unsigned long long m0 = v.gMask[g];
+  const int32_t fr = v.fReq[f], fl = v.fLim[f], fc = v.fCls[f], meta = v.iMeta[s];
+  const int32_t nact = v.h[H_NACT], sumu = v.h[H_SUMU];
+  if (n0 == 0) v.h[H_NACT] = nact + 1;
+  v.gMask[g] = m0 | (1ull << (fc & 63));
+  v.gR[g] = R0 + fr;
+  v.gL[g] = L0 + fl;
+  v.gU[g] = U0 + share;
+  v.h[H_SUMU] = sumu + share;
   const auto res = v.gRes + (size_t)g * RES;
-  int pos = v.gN[g];
+  int pos = n0;
+#if !DILU_HOT_SMEM
+  const auto rcl = v.gRcl + (size_t)g * RES;   // (wide layout) classes beside the residents
+#endif
   if (!(c.P->ovl | c.P->covl)) {   // keep (prio, id) order now ...
     const long long k = res_key(v, s);
     #pragma unroll 1
-    while (pos > 0 && res_key(v, res[pos - 1]) > k) { res[pos] = res[pos - 1]; --pos; }
+    while (pos > 0 && res_key(v, res[pos - 1]) > k) {
+      res[pos] = res[pos - 1];
+#if !DILU_HOT_SMEM
+      rcl[pos] = rcl[pos - 1];
+#endif
+      --pos;
+    }
   }                           // ... or append (overlapped slots: rows below gNs never move
   res[pos] = s;               // while P1 reads them; the next repack sorts the row)
-  v.gN[g] += 1;
-  const int32_t meta = v.iMeta[s];
+#if !DILU_HOT_SMEM
+  rcl[pos] = fc;
+#endif
+  v.gN[g] = n0 + 1;
   const int k0 = nst_of(meta);
   v.iG[s * MAXST + k0] = (int16_t)g;
   v.iShare[s * MAXST + k0] = share;
@@ -440,13 +457,24 @@ static __device__ DILU_SERIAL void release(Scn& c, int32_t s) {
     const int nr = v.gN[g];
     #pragma unroll 1
     while (j < nr && res[j] != s) ++j;
+#if !DILU_HOT_SMEM
+    const auto rcl = v.gRcl + (size_t)g * RES;
+    #pragma unroll 1
+    for (; j + 1 < nr; ++j) { res[j] = res[j + 1]; rcl[j] = rcl[j + 1]; }
+#else
     #pragma unroll 1
     for (; j + 1 < nr; ++j) res[j] = res[j + 1];
+#endif
     v.gN[g] = nr - 1;
     if (nr - 1 == 0) v.h[H_NACT] -= 1;
     unsigned long long m = 0;
+#if !DILU_HOT_SMEM
+    #pragma unroll 1
+    for (int x = 0; x < nr - 1; ++x) m |= 1ull << (rcl[x] & 63);
+#else
     #pragma unroll 1
     for (int x = 0; x < nr - 1; ++x) m |= 1ull << (v.fCls[v.iFunc[res[x]]] & 63);
+#endif
     v.gMask[g] = m;
     v.iG[s * MAXST + k] = -1;
   }
@@ -626,12 +654,19 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
     } else {
       const int32_t R = v.gR[g] + req, Lm = v.gL[g] + lim, U = v.gU[g] + mem;
       if (!(R <= c.om && Lm <= c.ga && U <= P.M && n < RES)) continue;
-      const auto res = v.gRes + (size_t)g * RES;
       // affinity: the class bitmask rules most GPUs out exactly; scan on a hit
       int aff = 0;
+#if !DILU_HOT_SMEM
+      const auto rcl = v.gRcl + (size_t)g * RES;   // one row of classes (wide layout)
+      if ((v.gMask[g] >> (cls & 63)) & 1ull)
+        #pragma unroll 1
+        for (int j = 0; j < n && !aff; ++j) aff = (rcl[j] == cls);
+#else
+      const auto res = v.gRes + (size_t)g * RES;
       if ((v.gMask[g] >> (cls & 63)) & 1ull)
         #pragma unroll 1
         for (int j = 0; j < n && !aff; ++j) aff = (v.fCls[v.iFunc[res[j]]] == cls);
+#endif
       const unsigned long long K = (unsigned long long)(aM * R + bQ * U);
       key = ((unsigned long long)(aff ? 0 : 1) << 62) | ((MASK40 - K) << 22) |
             (unsigned long long)g;
@@ -933,8 +968,16 @@ static __device__ void rebuild_layout(Scn& c) {
         const long long k = res_key(v, s);
         if (k > kp) { kp = k; continue; }
         int pos = j;
+#if !DILU_HOT_SMEM
+        const auto rcl = v.gRcl + (size_t)g * RES;
+        const int32_t cj = rcl[j];
+        #pragma unroll 1
+        while (pos > 0 && res_key(v, res[pos - 1]) > k) { res[pos] = res[pos - 1]; rcl[pos] = rcl[pos - 1]; --pos; }
+        rcl[pos] = cj;
+#else
         #pragma unroll 1
         while (pos > 0 && res_key(v, res[pos - 1]) > k) { res[pos] = res[pos - 1]; --pos; }
+#endif
         res[pos] = s;
       }
     }

@@ -74,6 +74,7 @@ struct Layout {
   size_t rB, bB, gB;       // per-batch-slot r, LLM stage minimum, training gang (B > 1 only)
   size_t aTc, aTm, aRl, aLe, aSt, aOw, aDt;   // literal Alg.2 state (cfg.flags bit2 only)
   size_t fSlo, iEmax, eB;  // request-level latency (cfg.flags bit3 only)
+  size_t gRcl;             // wide layout: each resident's affinity class, beside gRes
   size_t hot_bytes, bytes;
 };
 
@@ -147,6 +148,9 @@ inline Layout make_layout(int32_t G, int32_t F, int32_t I, int32_t W, int32_t B 
   L.fSlo = take(lat ? 4 * (size_t)F : 0);
   L.iEmax = take(lat ? 4 * 2 * (size_t)I : 0);
   L.eB = take(lat && B > 1 ? 4 * (size_t)B * I : 0);
+  // wide layout (state in HBM/L2): the affinity class of each row position, kept beside
+  // gRes so the placement's affinity test reads one row instead of res -> func -> class
+  L.gRcl = take(narrow ? 0 : 4 * (size_t)G * RES);
   L.bytes = align16(o);
   return L;
 }
@@ -248,6 +252,7 @@ template <bool N> struct ViewT {
   PI rB, bB, gB;
   PI aTc, aTm, aRl, aLe, aSt, aOw, aDt;
   PI fSlo, iEmax, eB;
+  PI gRcl;
   PI ring;  // global [F][W]
 };
 
@@ -316,6 +321,7 @@ inline ViewT<N> make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
   PT(int32_t, aSt, AG); PT(int32_t, aOw, AG); PT(int32_t, aDt, AG);
   PT(int32_t, fSlo, L.LT ? F : 0); PT(int32_t, iEmax, L.LT ? 2 * I : 0);
   PT(int32_t, eB, L.LT ? BB * I : 0);
+  PT(int32_t, gRcl, L.N ? 0 : G * RES);
 #undef PT
 #ifdef DILU_BOUNDS
   v.ring = Chk<int32_t>(nullptr, 0, id);   // set by the kernel (ring)
@@ -333,7 +339,7 @@ inline ViewT<N> make_view(uint8_t* hot, uint8_t* b, const Layout& L) {
   "fPat", "fScale", "fPhase", "fCap1", "fReg", "fNsamp", "fAcc", "fHead", "fUp", "fDown",      \
   "fThrn", "fOld", "fPv", "fNlive", "fLh", "fLt", "fGang", "fFlag", "fK", "fList", "fArr",     \
   "fDep", "fPidx", "fInfL", "fDefL", "qN", "qFail", "qSlot", "iQ", "rB",    \
-  "bB", "gB", "aTc", "aTm", "aRl", "aLe", "aSt", "aOw", "aDt", "fSlo", "iEmax", "eB", "ring",  \
+  "bB", "gB", "aTc", "aTm", "aRl", "aLe", "aSt", "aOw", "aDt", "fSlo", "iEmax", "eB", "gRcl", "ring",  \
   "members"
 
 }  // namespace dilu

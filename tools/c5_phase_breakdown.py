@@ -16,15 +16,19 @@ import dilu_inputs as di  # noqa: E402
 from paper_2503_05130_b200 import DiluSim, lib  # noqa: E402
 
 slots = int(sys.argv[1]) if len(sys.argv) > 1 else 3600
+burst = len(sys.argv) > 2 and sys.argv[2] == "burst"   # time the first 600 slots instead
 wl = di.c5(n_scenarios=8, T=slots, first_seed=50)
 sim = DiluSim.from_workload(wl)
-sim.scale_step(600)                      # past the initial fleet burst
+if burst:
+    slots = 1200
+else:
+    sim.scale_step(600)                  # past the initial fleet burst
 torch.cuda.synchronize()
 lib().dilu_sim_reset  # noqa
 per0 = np.zeros((8, 24), dtype=np.int64)
 lib().dilu_kernel_stats(sim.h, per0.ctypes.data, None)
 s0 = torch.cuda.Event(enable_timing=True); s1 = torch.cuda.Event(enable_timing=True)
-s0.record(); sim.scale_step(slots - 600); s1.record(); torch.cuda.synchronize()
+s0.record(); sim.scale_step(slots - 600); s1.record(); torch.cuda.synchronize()   # (burst: slots 0..599)
 per = np.zeros((8, 24), dtype=np.int64)
 lib().dilu_kernel_stats(sim.h, per.ctypes.data, None)
 d = (per - per0).sum(0)
