@@ -53,12 +53,14 @@ def raw(rep):
                 val *= 1e9
             elif u[i] == "Kbyte":
                 val *= 1e3
-            elif u[i] == "usecond":
+            elif u[i] in ("usecond", "us"):
                 val /= 1e3
-            elif u[i] == "nsecond":
+            elif u[i] in ("nsecond", "ns"):
                 val /= 1e6
-            elif u[i] == "second":
+            elif u[i] in ("second", "s"):
                 val *= 1e3
+            elif u[i] == "Tbyte":
+                val *= 1e12
             d[METRICS[n]] = val
         m = re.match(r"smsp__average_warps_issue_stalled_(\w+)_per_issue_active\.ratio", n)
         if m and m.group(1) in STALLS:
