@@ -379,9 +379,10 @@ dilu_status dilu_sim_create(const dilu_config* cfg, const dilu_scenario* h_scen,
         continue;
       }
       const int m_res = nclusters / S;           // clusters per scenario with every group resident
-      // groups beyond ~32 CTAs gained nothing on C5 (scenario-wide barriers cost more than
-      // the extra SMs save), so at most 32 unless DILU_GROUP asks; never more
-      // than fit at once -- the groups spin on their barriers
+      // groups beyond 32-64 CTAs lose on C5 (one C5 scenario: 1,229 / 1,199 / 1,399 / 1,747
+      // ms per step at 32 / 64 / 96 / 144 CTAs; 32 and 64 within box-to-box noise, DESIGN.md
+      // s5: scenario-wide barriers cost more than the extra SMs save), so at most 32 unless
+      // DILU_KCAP / DILU_GROUP ask; never more than fit at once -- the groups spin
       int cap = 32;                               // CTAs per scenario (tuning hook DILU_KCAP)
       if (const char* e = getenv("DILU_KCAP")) cap = atoi(e) > 0 ? atoi(e) : cap;
       int m = m_res < cap / kc ? m_res : (cap / kc > 0 ? cap / kc : 1);

@@ -27,6 +27,10 @@
 
 namespace dilu {
 
+// rare paths (capacity errors, LLM splits, lifecycle events, window recounts): laid out
+// away from the per-slot code, whose instruction footprint matters
+#define DILU_UNLIKELY(x) __builtin_expect(!!(x), 0)
+
 #ifndef DILU_HOT_SMEM
 #define DILU_HOT_SMEM 0
 #endif
@@ -552,8 +556,8 @@ static __device__ int32_t enqueue(Scn& c, int32_t f, int32_t n) {
 }
 static __device__ DILU_SERIAL int32_t enqueue_impl(Scn& c, int32_t f, int32_t n) {
   DILU_VIEW(v, c);
-  if (v.h[H_FSTOP] < n) { v.h[H_ERR] = 6; return -1; }
-  if (v.h[H_QLEN] == c.P->I) {
+  if (DILU_UNLIKELY(v.h[H_FSTOP] < n)) { v.h[H_ERR] = 6; return -1; }
+  if (DILU_UNLIKELY(v.h[H_QLEN] == c.P->I)) {
     compact_queue(c);
     v.h[H_QNEWPOS] = 0;               // positions moved: the next pass scans everything
   }
@@ -680,7 +684,7 @@ static __device__ bool place_one(Scn& c, Red& red, int& ph, int32_t s) {
     PG::sync(c);
     return true;
   }
-  if (v.fKind[f] == K_LLM && (P.flags & 1) && c.mode != M_EXCLUSIVE) {
+  if (DILU_UNLIKELY(v.fKind[f] == K_LLM && (P.flags & 1) && c.mode != M_EXCLUSIVE)) {
     // worst-fit split: repeated argmax of free memory over active, cap-feasible GPUs
     int32_t picked[MAXST];
     int32_t pfree[MAXST];
@@ -755,7 +759,7 @@ static __device__ DILU_SERIAL bool hope_after(const Scn& c, int32_t fe, int32_t 
   DILU_CVIEW(v, c);
   const int32_t n = v.h[H_RLN];
   const int32_t lo = n > RLOG ? n - RLOG : 0;
-  if (n > RLOG && v.rlE[lo % RLOG] > fe) {
+  if (DILU_UNLIKELY(n > RLOG && v.rlE[lo % RLOG] > fe)) {
     #pragma unroll 1
     for (int32_t g = 0; g < c.P->G; ++g)
       if (v.gRel[g] > fe && could_help(c, g, f)) return true;
@@ -885,12 +889,17 @@ static __device__ void placement_pass(Scn& c, Red& red, int& ph, int32_t t, Acc&
         c.flag[0] = e;
         c.flag[1] = qn;
         if (e < qn) {                   // gang members, ascending id
-          const int32_t n = v.qN[e], s0 = v.qSlot[e], f = v.iFunc[s0], first = v.iId[s0];
-          int j = 0;
-          #pragma unroll 1
-          for (int32_t s = v.fLh[f]; s >= 0 && j < n; s = v.iNext[s]) {
-            const int32_t id = v.iId[s];
-            if (id >= first && id < first + n) c.members[j++] = s;
+          const int32_t n = v.qN[e], s0 = v.qSlot[e];
+          if (n == 1) {
+            c.members[0] = s0;          // a single instance: the queue holds its slot
+          } else {
+            const int32_t f = v.iFunc[s0], first = v.iId[s0];
+            int j = 0;
+            #pragma unroll 1
+            for (int32_t s = v.fLh[f]; s >= 0 && j < n; s = v.iNext[s]) {
+              const int32_t id = v.iId[s];
+              if (id >= first && id < first + n) c.members[j++] = s;
+            }
           }
           acc.z->st[S_ATTEMPT] += 1;
         }
@@ -1819,9 +1828,9 @@ static __device__ int32_t b1_func(Scn& c, int32_t f, int32_t sec) {
         v.fNsamp[f] = ns < W ? ns + 1 : W;     // saturating: only >= W / >= 1 matter
         v.fAcc[f] = 0;
       }
-      if (v.fDep[f] == sec) {                     // step 2: departure
+      if (DILU_UNLIKELY(v.fDep[f] == sec)) {      // step 2: departure
         ev = EV_DEP;
-      } else if (inf && c.mode == M_EAGER) {      // reactive scaling on the last sample
+      } else if (DILU_UNLIKELY(inf && c.mode == M_EAGER)) {   // reactive scaling on the last sample
         if (v.fNsamp[f] >= 1) {
           const int32_t n = v.fNlive[f];
           if ((long long)last > (long long)n * cap1) {
@@ -1834,12 +1843,12 @@ static __device__ int32_t b1_func(Scn& c, int32_t f, int32_t sec) {
       } else if (inf && v.fNsamp[f] >= W) {       // step 3: lazy scaling decision
         const int32_t n = v.fNlive[f];
         const long long cu = (long long)n * cap1, cd = (long long)(n - 1) * cap1;
-        if (v.fThrn[f] != n) {
+        if (DILU_UNLIKELY(v.fThrn[f] != n)) {
           int32_t up = 0, dn = 0;
           for (int j = 0; j < W; ++j) { const int32_t w = ring[j]; up += w > cu; dn += w < cd; }
           v.fUp[f] = up; v.fDown[f] = dn; v.fThrn[f] = n;
         }
-        if (v.fUp[f] >= P.phi_out) {
+        if (DILU_UNLIKELY(v.fUp[f] >= P.phi_out)) {
           int32_t mx = 0;
           for (int j = 0; j < W; ++j) mx = max(mx, ring[j]);
           const long long k = ((long long)mx + cap1 - 1) / cap1 - n;
@@ -1849,7 +1858,7 @@ static __device__ int32_t b1_func(Scn& c, int32_t f, int32_t sec) {
         }
       }
     }
-    if (v.fArr[f] == sec) ev |= EV_ARR;           // step 4: arrival
+    if (DILU_UNLIKELY(v.fArr[f] == sec)) ev |= EV_ARR;   // step 4: arrival
   }
   v.fFlag[f] = ev;
   return ev;

@@ -29,6 +29,10 @@ METRICS = {
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "smem_wavefronts",
     "lts__t_bytes.sum": "l2_bytes",
     "sm__cycles_elapsed.avg": "sm_cycles",
+    # regime reporting: L2 and DRAM throughput as % of peak
+    "lts__throughput.sum.pct_of_peak_sustained_elapsed": "l2_throughput_pct",
+    "lts__t_sectors.sum.pct_of_peak_sustained_elapsed": "l2_sectors_pct",
+    "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed": "memory_throughput_pct",
 }
 STALLS = ["barrier", "long_scoreboard", "short_scoreboard", "wait", "no_instruction", "selected",
           "not_selected", "math_pipe_throttle", "mio_throttle", "branch_resolving", "lg_throttle",
@@ -69,6 +73,8 @@ def raw(rep):
             except ValueError:
                 pass
     d["dram_bytes_per_launch"] = d.get("dram_read_bytes", 0) + d.get("dram_write_bytes", 0)
+    if d.get("duration_ms"):
+        d["dram_gbs"] = d["dram_bytes_per_launch"] / d["duration_ms"] / 1e6   # achieved DRAM GB/s
     st = d.get("stall_per_issue", {})
     tot = sum(st.values()) or 1.0
     d["stall_share_pct"] = {k: round(100 * x / tot, 1) for k, x in sorted(st.items(), key=lambda kv: -kv[1]) if x > 0}
