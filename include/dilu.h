@@ -85,7 +85,10 @@ typedef struct {
   int32_t flags;              /* bit0: LLM worst-fit split enabled; bit2: literal Alg.2 at */
                               /* 5 ms periods (D8) instead of   */
                               /* the slot-level grant; needs slot_ms % 5 == 0; bit3: request- */
-                              /* level latency (dilu_latency, D10); bit1 unused               */
+                              /* level latency (dilu_latency, D10); bit1: device state      */
+                              /* invariants I1-I3, I7 checked after every scale_step /       */
+                              /* place_batch, I6 in dilu_metrics; */
+                              /* a violation is reported as DILU_E_INVARIANT by dilu_metrics */
 } dilu_config;
 
 /* Per-scenario parameters (the C4 sweep varies gamma per scenario). */

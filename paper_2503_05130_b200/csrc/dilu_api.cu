@@ -542,6 +542,16 @@ dilu_status dilu_sim_reset(dilu_sim* s) {
   return cuda_check(s, cudaGetLastError(), "k_init launch");
 }
 
+// cfg.flags bit1: the state invariants after every call (k_check)
+static dilu_status launch_check(dilu_sim* s) {
+  if (!(s->cfg.flags & 2)) return DILU_OK;
+  if (s->L.N)
+    k_check<true><<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P);
+  else
+    k_check<false><<<s->cfg.n_scenarios, 256, 0, s->stream>>>(s->P);
+  return cuda_check(s, cudaGetLastError(), "k_check launch");
+}
+
 dilu_status dilu_place_batch(dilu_sim* s, int32_t n_req, const int32_t* d_req_scenario,
                              const int32_t* d_req_func, int32_t* d_out_gpu, int32_t* d_out_iid) {
   if (!s) return DILU_E_USAGE;
@@ -566,7 +576,8 @@ dilu_status dilu_place_batch(dilu_sim* s, int32_t n_req, const int32_t* d_req_sc
       if (!ok) return fail(s, DILU_E_USAGE, "place_batch: request %d names an invalid scenario/function", j);
     }
   }
-  return launch_run(s, 0, n_req, d_req_scenario, d_req_func, d_out_gpu, d_out_iid);
+  const dilu_status rc = launch_run(s, 0, n_req, d_req_scenario, d_req_func, d_out_gpu, d_out_iid);
+  return rc == DILU_OK ? launch_check(s) : rc;
 }
 
 dilu_status dilu_scale_step(dilu_sim* s, int32_t n_slots) {
@@ -576,6 +587,7 @@ dilu_status dilu_scale_step(dilu_sim* s, int32_t n_slots) {
   if (n_slots == 0) return DILU_OK;
   dilu_status rc = launch_run(s, n_slots, -1, nullptr, nullptr, nullptr, nullptr);
   if (rc == DILU_OK) s->t += n_slots;
+  if (rc == DILU_OK) rc = launch_check(s);
   return rc;
 }
 
@@ -599,7 +611,11 @@ dilu_status dilu_metrics(dilu_sim* s, int64_t* per_scenario, int64_t* sum) {
   if (host_sum[NT] == DILU_E_CAPACITY)
     return fail(s, DILU_E_CAPACITY, "a scenario exceeded max_instances=%d live instances",
                 s->cfg.max_instances);
+  if (host_sum[NT] == 2)
+    return fail(s, DILU_E_INVARIANT, "a state invariant (I1/I2/I3/I7) failed on the device");
   if (host_sum[NT] != 0) return fail(s, DILU_E_INVARIANT, "scenario error code %lld", (long long)host_sum[NT]);
+  if ((s->cfg.flags & 2) && host_sum[T_RTOT] != host_sum[T_RSRV] + host_sum[T_RVIO])   // I6
+    return fail(s, DILU_E_INVARIANT, "I6: requests total != served + violated");
   return DILU_OK;
 }
 

@@ -414,7 +414,7 @@ static __device__ DILU_SERIAL void commit(Scn& c, int32_t s, int32_t g, int32_t 
 #if !DILU_HOT_SMEM
   const auto rcl = v.gRcl + (size_t)g * RES;   // (wide layout) classes beside the residents
 #endif
-  if (!(c.P->ovl | c.P->covl)) {   // keep (prio, id) order now ...
+  if (DILU_UNLIKELY(!(c.P->ovl | c.P->covl))) {   // keep (prio, id) order now ...
     const long long k = res_key(v, s);
     #pragma unroll 1
     while (pos > 0 && res_key(v, res[pos - 1]) > k) {
@@ -434,7 +434,7 @@ static __device__ DILU_SERIAL void commit(Scn& c, int32_t s, int32_t g, int32_t 
   v.iG[s * MAXST + k0] = (int16_t)g;
   v.iShare[s * MAXST + k0] = share;
   if (k0 == 0) v.iSh0[s] = share;
-  if (c.P->flags & 4) {       // Alg.2 stage state starts fresh (D8)
+  if (DILU_UNLIKELY(c.P->flags & 4)) {   // Alg.2 stage state starts fresh (D8)
     const int32_t e = s * MAXST + k0;
     v.aTc[e] = 0; v.aTm[e] = 0; v.aRl[e] = 0; v.aLe[e] = A2_NEVER;
   }
@@ -1308,7 +1308,7 @@ static __device__ void phase2(Scn& c, int32_t t, Acc& acc) {
     } else {
       for (int32_t s = lh[f]; s >= 0; s = nxt[s]) {
         const int32_t nst = nst_of(meta[s]);
-        if (nst <= 1) continue;                 // unsplit: finished in P1
+        if (__builtin_expect(nst <= 1, 1)) continue;   // unsplit: finished in P1
         const int32_t b = bmin[s];
         if (b == BIG) continue;
         bmin[s] = BIG;
@@ -2488,6 +2488,66 @@ __global__ void k_init(Params P) {
 }
 
 // Snapshot for parity tests (off the timed path).
+// State invariants (cfg.flags bit1), checked on the device
+// at the end of every dilu_scale_step / dilu_place_batch call, one CTA per scenario:
+//   I1  R_g <= Omega_u, L_g <= gamma_u, U_g <= M, |res_g| <= 32 (Eq.4)
+//   I2  the active count equals #{g : res_g != {}}, the memory total equals sum_g U_g (Eq.5)
+//   I3  R_g, L_g, U_g equal the sums over the residents of g (their stage shares)
+//   I7  a placed instance has 1..4 stage GPUs, distinct, each listing it (Eq.2)
+// A violation sets the scenario's error word to DILU_E_INVARIANT (2), which dilu_metrics
+// reports; I6 (requests total = served + violated) is checked there on the tallies.
+template <bool N>
+__global__ void k_check(Params P) {
+  const int32_t sc = blockIdx.x;
+  uint8_t* blk = P.state + (size_t)sc * P.L.bytes;
+  const ViewT<N> v = make_view<N>(blk, blk, P.L);
+  const int32_t om = P.scen[sc * 4 + 1], ga = P.scen[sc * 4 + 2];
+  __shared__ int bad;
+  __shared__ unsigned long long act, sumu;
+  if (threadIdx.x == 0) { bad = 0; act = 0; sumu = 0; }
+  __syncthreads();
+  if (v.h[H_ERR]) return;                        // an earlier error stands
+  for (int32_t g = threadIdx.x; g < P.G; g += blockDim.x) {
+    const int32_t n = v.gN[g];
+    long long R = 0, L = 0, U = 0;
+    bool ok = n >= 0 && n <= RES && v.gR[g] <= om && v.gL[g] <= ga && v.gU[g] <= P.M;   // I1
+    for (int32_t j = 0; ok && j < n; ++j) {
+      const int32_t s = v.gRes[(size_t)g * RES + j];
+      if (s < 0 || s >= P.I || st_of(v.iMeta[s]) != ST_PLACED) { ok = false; break; }
+      const int32_t f = v.iFunc[s], ns = nst_of(v.iMeta[s]);
+      R += v.fReq[f]; L += v.fLim[f];
+      int hits = 0;
+      for (int k = 0; k < ns; ++k)
+        if (v.iG[s * MAXST + k] == g) { U += k == 0 ? v.iSh0[s] : v.iShare[s * MAXST + k]; ++hits; }
+      ok &= hits == 1;                           // listed on g exactly once among its stages
+    }
+    ok &= R == v.gR[g] && L == v.gL[g] && U == v.gU[g];                                   // I3
+    if (!ok) atomicOr(&bad, 1);
+    if (n > 0) atomicAdd(&act, 1ull);
+    atomicAdd(&sumu, (unsigned long long)(long long)v.gU[g]);
+  }
+  for (int32_t s = threadIdx.x; s < P.I; s += blockDim.x) {                              // I7
+    const int32_t meta = v.iMeta[s];
+    if (st_of(meta) != ST_PLACED) continue;
+    const int32_t ns = nst_of(meta);
+    bool ok = ns >= 1 && ns <= MAXST;
+    for (int k = 0; ok && k < ns; ++k) {
+      const int32_t g = v.iG[s * MAXST + k];
+      ok = g >= 0 && g < P.G;
+      for (int k2 = 0; ok && k2 < k; ++k2) ok = v.iG[s * MAXST + k2] != g;
+      bool listed = false;
+      for (int32_t j = 0; ok && j < v.gN[g] && !listed; ++j) listed = v.gRes[(size_t)g * RES + j] == s;
+      ok &= listed;
+    }
+    if (!ok) atomicOr(&bad, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (act != (unsigned long long)v.h[H_NACT] || (long long)sumu != (long long)v.h[H_SUMU]) bad = 1;   // I2
+    if (bad) v.h[H_ERR] = 2;
+  }
+}
+
 template <bool N>
 __global__ void k_snapshot(Params P, int32_t id_cap, int32_t* out_gpu, int32_t* out_inst) {
   const int32_t sc = blockIdx.x;

@@ -511,3 +511,51 @@ def test_multicluster_groups(shape, monkeypatch):
     run_pair(di.c2(seed=7, T=600), [1, 299, 300], id_cap=4096)
     wl = di.scaled("C5g", 2048, 200, 400, 1200, 100, 900, [52, 53], max_instances=8192)
     run_pair(wl, [1, 13, 886], id_cap=8192, snap=False)
+
+
+# ---- device state invariants (cfg.flags bit1) ---------------
+
+@pytest.mark.parametrize("case", ["c1", "c2", "c4slice_modes", "c5r", "llm_split", "alg2"])
+def test_invariant_checks_clean(case, monkeypatch):
+    """With cfg.flags bit1 the device checks I1-I3 and I7 after every call and dilu_metrics
+    checks I6; on the paper's loop none may fire, and the tallies stay those of the oracle
+    (which runs its own per-slot checks with the same bit)."""
+    if case == "c1":
+        wl, chunks = di.c1(), [1] * 30 + [70]
+    elif case == "c2":
+        wl, chunks = di.c2(seed=2, T=600), [1, 1, 98, 500]
+    elif case == "c4slice_modes":
+        base = di.c4(n_scenarios=4096, T=300).subset(np.arange(3, 4096, 257))
+        wl, chunks = di.with_modes(base, np.arange(base.S) % 5), [1, 299]
+    elif case == "c5r":
+        monkeypatch.setenv("DILU_ENGINE", "cluster")
+        wl, chunks = di.scaled("C5i", 2048, 200, 400, 1200, 100, 600, [54], max_instances=8192), [1, 9, 590]
+    elif case == "llm_split":     # the C4 sweep points with worst-fit splits (test_llm_split_heavy)
+        wl, chunks = di.c4(n_scenarios=4096, T=300).subset(np.arange(0, 640, 61)), [1, 299]
+    else:
+        wl, chunks = with_flags(di.c2(seed=4, T=300), 4), [1, 299]
+    run_pair(with_flags(wl, 2), chunks, snap=False)
+
+
+def test_invariant_violation_detected():
+    """A corrupted GPU row (R_g one above the sum over its residents) is reported as
+    DILU_E_INVARIANT by the next call's device check (I3)."""
+    from paper_2503_05130_b200 import DiluError
+    wl = with_flags(di.c2(seed=1, T=200), 2)
+    gs = gpu_sim(wl)
+    gs.scale_step(100)
+    gs.metrics()                                          # clean so far
+    gg, _ = gs.snapshot(1)
+    R = gg.cpu().numpy()[0, :, 0].astype(np.int32)        # this scenario's R_g row
+    g = int(np.argmax(R))
+    assert R[g] > 0
+    import torch
+    ws = gs.workspace.view(torch.int32)
+    W = ws.cpu().numpy()
+    hits = np.flatnonzero(np.all(np.lib.stride_tricks.sliding_window_view(W, R.size) == R, axis=1))
+    assert hits.size >= 1                                 # the gR array of the state block
+    ws[int(hits[0]) + g] += 1
+    gs.scale_step(1)
+    with pytest.raises(DiluError) as e:
+        gs.metrics()
+    assert e.value.code == 2                              # DILU_E_INVARIANT
