@@ -172,7 +172,9 @@ dilu_status dilu_scale_step(dilu_sim* s, int32_t n_slots);
  * Reduce tallies: per-scenario int64 [n_scenarios][DILU_NT] (may be NULL) and the
  * scenario sum int64 [DILU_NT] (uint64 wrap-sum for the hash, may be NULL).  Pointers
  * may be host or device (copied with cudaMemcpyDefault).  Synchronises the stream and
- * returns any deferred DILU_E_CAPACITY / DILU_E_CUDA. */
+ * returns any deferred DILU_E_CAPACITY / DILU_E_CUDA, and with cfg.flags bit1 a failed
+ * device state invariant (I1-I3, I7, checked after every scale_step / place_batch) or
+ * I6 on the tallies as DILU_E_INVARIANT. */
 dilu_status dilu_metrics(dilu_sim* s, int64_t* per_scenario, int64_t* sum);
 
 /* Parity helper (off the timed path): device outputs

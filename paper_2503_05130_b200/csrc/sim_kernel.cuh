@@ -576,9 +576,12 @@ static __device__ DILU_SERIAL int32_t enqueue_impl(Scn& c, int32_t f, int32_t n)
     if (j == 0) v.qSlot[q] = s;
     #pragma unroll 1
     for (int k = 0; k < MAXST; ++k) v.iG[s * MAXST + k] = -1;
-    v.iBmin[s] = BIG;
-    v.iBmin[c.P->I + s] = BIG;
-    if (c.P->SPS == 1) v.iR[c.P->I + s] = BIG;   // stage-minimum half of iR (phase1)
+    if (c.P->SPS == 1) {
+      v.iR[c.P->I + s] = BIG;         // stage-minimum half of iR (phase1); iBmin unused
+    } else {
+      v.iBmin[s] = BIG;
+      v.iBmin[c.P->I + s] = BIG;
+    }
     list_append(v, f, s);
     v.fNlive[f] += 1;
     v.h[H_NLIVE] += 1;
