@@ -1963,7 +1963,12 @@ static __device__ bool boundary(Scn& c, Red& red, int& ph, int32_t t, Acc& acc, 
     for (int32_t e = 0; e < total; ++e) {     // step 2: departures
       const int32_t f = v.fList[e];
       if (!(v.fFlag[f] & EV_DEP)) continue;
-      kill_queue_entries_of(c, f);
+      // a live queue entry holds pending instances of its function: scan the queue only if
+      // f has one (its list is short, the queue is not)
+      bool pend = false;
+      #pragma unroll 1
+      for (int32_t s = v.fLh[f]; s >= 0 && !pend; s = v.iNext[s]) pend = st_of(v.iMeta[s]) == ST_PEND;
+      if (pend) kill_queue_entries_of(c, f);
       while (v.fLh[f] >= 0) terminate(c, v.fLh[f]);
       v.fReg[f] = 0;
     }
