@@ -29,11 +29,11 @@ enum : int32_t { ST_FREE = 0, ST_PEND = 1, ST_PLACED = 2 };
 // header slots (int32)
 enum : int {
   H_NEXT_IID = 0, H_NLIVE, H_QLEN, H_NACT, H_SUMU, H_EPOCH, H_DIRTY, H_FSTOP, H_ERR,
-  H_NEV, H_CCNT = 10 /*6*/, H_CBASE = 16 /*7*/, H_GBASE = 23 /*6*/, H_CCNT2 = 29 /*6*/,
+  H_NEV /* events of the current boundary (prerecount_warp) */, H_CCNT = 10 /*6*/, H_CBASE = 16 /*7*/, H_GBASE = 23 /*6*/, H_CCNT2 = 29 /*6*/,
   H_RLN = 35 /* release-log entries appended */, H_NINF = 36, H_NDEF = 37,
   H_QLIVE = 38 /* live queue requests */, H_LASTEP = 39 /* release epoch at the last pass's end */,
   H_QNEWPOS = 40 /* first request enqueued since the last pass, -1 if none */,
-  H_PNEV = 41 /* pipelined slots: events of the next boundary (b1_warp) */, H_WORDS = 44
+  H_SPARE = 41 /* unused */, H_WORDS = 44
 };
 
 // tally indices (match include/dilu.h)
