@@ -2,7 +2,7 @@
 # library), smoke, bench lines, ncu launch list and full captures, phase breakdowns.
 # Run: gpurun -- bash tools/collect_r2.sh   (compute-sanitizer is closed on this pool)
 set -x
-D=gpurun_out/r2final2
+D=gpurun_out/r2final
 mkdir -p $D
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > $D/gpu.txt
 timeout 1500 python -m pytest tests -m gpu -q > $D/pytest_gpu.txt 2>&1; echo "rc $?" >> $D/pytest_gpu.txt
